@@ -1,0 +1,208 @@
+/*
+ * pg.h — C ABI of the B200-native greedy all-switches strategy improvement
+ * library (Fearnley, "Efficient Parallel Strategy Improvement for Parity
+ * Games", arXiv 1705.02313). Library: paper_1705_02313_b200/libpgsi.so.
+ *
+ * The problem (§2): given a parity game
+ * G = (V, V_Even, V_Odd, E, pri), compute the winning partition
+ * (W_Even, W_Odd) together with positional strategies for both players.
+ * The method is Algorithm 1: an outer greedy all-switches
+ * improvement loop for Even around an inner
+ * one-player strategy-improvement loop for Odd that computes the best
+ * response br(σ). Every inner iteration computes
+ * a valuation val^{σ,τ} of the current profile — the
+ * data-parallel hot path — on the GPU.
+ *
+ * General conventions
+ *  - Every call is synchronous: when it returns, outputs are written (and, in
+ *    device-pointer mode, the work on the handle's stream has completed).
+ *  - No exception crosses the ABI. Every call returns a pg_status; on failure
+ *    pg_last_error() returns a thread-local message naming the first offending
+ *    index or the failing CUDA call.
+ *  - Ownership: the caller owns every buffer it passes. Inputs are copied on
+ *    entry and no caller pointer is retained after a call returns. Outputs are
+ *    caller-allocated. A pg_game handle owns its device memory until pg_free.
+ *  - Pointer kind: host pointers by default. If the handle was loaded with
+ *    PG_PTRS_ON_DEVICE, the strategy/val/top/winner/... pointers of
+ *    pg_valuate, pg_best_response and pg_solve are device pointers (e.g. a
+ *    torch tensor's data_ptr()) on the handle's device; pg_load's inputs are
+ *    always host pointers.
+ *  - Vertex numbering ("ABI order"): the handle holds the preprocessed game
+ *    (PAPER.md:406-413). Internal-facing calls (pg_valuate, pg_best_response)
+ *    use n_internal = n + dummies entries: the n original vertices in input
+ *    order, then the dummies (dummy n+k belongs to the k-th preprocessed
+ *    vertex in increasing id order). pg_solve outputs have n entries.
+ *  - Strategies: entry v is the successor chosen at v. PG_SINK (-1) means the
+ *    edge to the sink s added for every Even vertex; only
+ *    Even vertices (including dummies) may choose it. Output arrays write
+ *    PG_NONE (-2) at vertices of the other player.
+ *  - Valuations: row-major int32 [n_rows][d] COUNTS: val[v*d+i] = number of
+ *    vertices with priority D[i] on the play from v to the sink, v included,
+ *    sink excluded; D = pg_info's sorted priorities, so the
+ *    highest priority is the last column. Rows of ⊤ vertices (infinite
+ *    plays) are written as zeros and flagged in top[].
+ *  - Priorities: any value >= 0 is accepted (PGSolver uses 0; the paper says
+ *    "positive"); parity is that of the value. Priorities are
+ *    only re-indexed, never merged.
+ */
+#ifndef PG_H_
+#define PG_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pg_game_s *pg_game;
+
+typedef enum {
+    PG_OK = 0,
+    PG_EINVAL = -1,         /* malformed input: CSR, terminal vertex,
+                               out-of-range successor, owner not in {0,1}, priority < 0,
+                               strategy entry that is not an edge, NULL required pointer */
+    PG_ENOMEM = -2,         /* host or device allocation failed */
+    PG_ECUDA = -3,          /* a CUDA runtime call failed (message names it) */
+    PG_ENCCL = -4,          /* reserved: multi-GPU communication failure */
+    PG_EINADMISSIBLE = -5,  /* an odd-dominated cycle appeared while computing a best
+                               response: σ is not admissible */
+    PG_EITERCAP = -6,       /* max_inner / max_outer cap exceeded */
+    PG_ESTATE = -7,         /* handle unusable after an earlier fatal CUDA error */
+    PG_ENOTSUP = -8         /* unsupported size (e.g. > 2^31-2 internal vertices) */
+} pg_status;
+
+#define PG_SINK (-1)
+#define PG_NONE (-2)
+
+/* pg_options.flags */
+enum {
+    PG_NO_PREPROCESS = 1,     /* skip admissibility preprocessing; an
+                                 inadmissible σ_init then yields PG_EINADMISSIBLE       */
+    PG_CHECK_INVARIANTS = 2,  /* check every valuation for odd cycles (admissibility)    */
+    PG_PHASE_TIMING = 4,      /* record CUDA events per phase; filled into pg_stats      */
+    PG_PTRS_ON_DEVICE = 8     /* valuate/best_response/solve pointers are device pointers */
+};
+
+typedef struct {
+    uint32_t flags;       /* PG_* flags above                                          */
+    int32_t device;       /* CUDA device ordinal                                       */
+    void *stream;         /* cudaStream_t to run on; NULL = the handle creates its own */
+    int32_t splitter_k;   /* V2 splitter depth stride (0 = default 32; 1..255)          */
+    int32_t reserved;
+    int64_t max_inner;    /* cap on total inner iterations per call (0 = none)         */
+    int64_t max_outer;    /* cap on outer passes per pg_solve (0 = none)               */
+} pg_options;
+
+typedef struct {
+    int64_t n, n_internal, m, m_internal, d, dummies;
+    int64_t inner_iters;     /* valuations computed = "Tot." of Table 3 (reading 12)      */
+    int64_t outer_passes;    /* best responses computed incl. the final no-switch pass
+                                (SURVEY.md §8(c) reading 11)                              */
+    int64_t odd_switches, even_switches;  /* total edges switched                         */
+    int64_t v1_rounds;       /* pointer-jumping rounds summed over valuations              */
+    int64_t v2_split_valuations; /* valuations that needed the splitter (deep) path        */
+    int64_t max_depth;       /* deepest finite play seen                                   */
+    int64_t gpu_launches;    /* kernels launched by the call                               */
+    double ms_load, ms_call;             /* host wall time of pg_load / of the last call   */
+    double ms_v1, ms_v2, ms_odd, ms_even, ms_other; /* PG_PHASE_TIMING: CUDA-event totals */
+    int64_t n_v1, n_v2, n_odd, n_even;   /* PG_PHASE_TIMING: launches per phase            */
+    /* algorithmic HBM bytes summed over the call:
+     * V1   = 5·n'             (succ read, ⊤ flag write)
+     * V2   = n' + R·n_fin     (priority index read, one row write per finite vertex)
+     * odd  = 4(n_odd+1) + 4·n_odd + (4+1)·m_odd + n_odd + R·rows_odd + 4·switched
+     * even = 4(n_even+1) + 4·n_even + (4+1)·m_even + n_even + R·rows_even + 4·switched
+     * with R = 4·dp row bytes and rows_* = finite non-sink rows the kernel gathered. */
+    double bytes_v1, bytes_v2, bytes_odd, bytes_even;
+} pg_stats;
+
+/* pg_load: validate, canonicalise and preprocess a game, copy it to the GPU.
+ *   n            number of vertices (>= 0)
+ *   row_ptr      host int64[n+1]; row_ptr[0] = 0, row_ptr[v] < row_ptr[v+1]
+ *                (every vertex needs an out-edge)
+ *   col          host int32[row_ptr[n]]; successors in [0, n); duplicates allowed and
+ *                removed; order is irrelevant (adjacency is sorted by id: reading 3)
+ *   owner        host uint8[n]; 0 = Even, 1 = Odd
+ *   priority     host int32[n]; >= 0
+ *   opt          options (NULL = defaults: device 0, own stream, preprocessing on)
+ *   out          receives the handle
+ * Errors: PG_EINVAL (message names the first offending index), PG_ENOMEM,
+ * PG_ECUDA, PG_ENOTSUP. */
+pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col,
+                  const uint8_t *owner, const int32_t *priority,
+                  const pg_options *opt, pg_game *out);
+
+/* pg_info: sizes of the loaded (preprocessed) game. Any output may be NULL.
+ *   priorities   int32[d] receives D sorted ascending (host pointer always). */
+pg_status pg_info(pg_game g, int64_t *n_internal, int32_t *d, int32_t *priorities,
+                  int64_t *dummies);
+
+/* pg_valuate: val^{σ,τ} of an arbitrary profile (reading 17).
+ *   strategy     int32[n_internal]: σ(v) for Even v (PG_SINK allowed), τ(v) for Odd v
+ *   val          int32[n_internal*d] or NULL: counts (rows of ⊤ vertices = 0)
+ *   top          uint8[n_internal] or NULL: 1 iff val(v) = ⊤ (infinite play)
+ *   cycle_dom    int32[n_internal] or NULL: for ⊤ v the largest priority on the cycle
+ *                the play from v reaches; -1 for finite v
+ * Errors: PG_EINVAL if an entry is not an edge. Odd cycles are NOT an error here. */
+pg_status pg_valuate(pg_game g, const int32_t *strategy, int32_t *val, uint8_t *top,
+                     int32_t *cycle_dom);
+
+/* pg_best_response: br(σ) by one-player greedy all-switches SI for Odd
+ * (Algorithm 1 inner loop PAPER.md:554-557).
+ *   sigma        int32[n_internal]; Even entries are σ, Odd entries ignored
+ *   tau0         int32[n_internal] or NULL: starting τ (Odd entries); NULL = first
+ *                successor (reading 4)
+ *   tau_out      int32[n_internal] or NULL: τ at exit (PG_NONE at Even vertices)
+ *   val, top     as pg_valuate, for the profile (σ, τ_out), i.e. val^σ
+ *   inner_iters  int64* or NULL: valuations computed
+ * Errors: PG_EINVAL, PG_EINADMISSIBLE (odd cycle reached), PG_EITERCAP. */
+pg_status pg_best_response(pg_game g, const int32_t *sigma, const int32_t *tau0,
+                           int32_t *tau_out, int32_t *val, uint8_t *top,
+                           int64_t *inner_iters);
+
+/* pg_solve: Algorithm 1 from σ_init (σ(v) = s) on the device.
+ *   winner       uint8[n]: 0 if v ∈ W_Even (val^{σ*}(v) = ⊤), 1 if v ∈ W_Odd
+ *
+ *   sigma        int32[n] or NULL: σ*(v) for Even v (PG_SINK possible only on W_Odd),
+ *                PG_NONE for Odd v
+ *   tau          int32[n] or NULL: τ* = br(σ*) for Odd v, a dummy successor w_x
+ *                reported as x (projection to original edges); PG_NONE for Even v
+ *   val          int32[n*d] or NULL: counts of val^{σ*} for the original vertices
+ *   stats        pg_stats* or NULL
+ * Errors: PG_EINADMISSIBLE (only possible with PG_NO_PREPROCESS), PG_EITERCAP,
+ * PG_ECUDA. */
+pg_status pg_solve(pg_game g, uint8_t *winner, int32_t *sigma, int32_t *tau,
+                   int32_t *val, pg_stats *stats);
+
+/* pg_inspect: run pg_load's host-side transform only (validation, canonical
+ * adjacency, preprocessing, priority indexing; §8(a1)) without touching a GPU, and
+ * report the internal game in ABI order. Two-call pattern: pass NULL arrays to
+ * get the sizes, then buffers of n_internal (+1) / m_internal entries.
+ *   flags                 PG_NO_PREPROCESS honoured, other bits ignored
+ *   owner_int  uint8[n_internal]      0 Even / 1 Odd (dummies are Even)
+ *   pidx_int   int32[n_internal]      index of the vertex priority in D
+ *   adj_ptr    int64[n_internal+1]    canonical adjacency offsets
+ *   adj        int32[m_internal]      successors (ABI ids); the sink is implicit
+ *   priorities int32[d]               D sorted ascending
+ * Errors: as pg_load's validation (PG_EINVAL, PG_ENOTSUP). */
+pg_status pg_inspect(int64_t n, const int64_t *row_ptr, const int32_t *col,
+                     const uint8_t *owner, const int32_t *priority, uint32_t flags,
+                     int64_t *n_internal, int32_t *d, int64_t *dummies, int64_t *m_internal,
+                     uint8_t *owner_int, int32_t *pidx_int, int64_t *adj_ptr, int32_t *adj,
+                     int32_t *priorities);
+
+/* pg_get_stats: statistics of the last call on the handle (host pointer). */
+pg_status pg_get_stats(pg_game g, pg_stats *stats);
+
+/* pg_free: release the handle and its device memory (NULL is a no-op). */
+void pg_free(pg_game g);
+
+/* pg_last_error: thread-local message for the last failing call on this thread. */
+const char *pg_last_error(void);
+
+/* pg_version: library version string. */
+const char *pg_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PG_H_ */

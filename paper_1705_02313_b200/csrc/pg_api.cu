@@ -1,0 +1,634 @@
+// pg_api.cu — the C ABI (include/pg.h): handle, device memory, and the host
+// driver of Algorithm 1. All arithmetic of the path runs in
+// the kernels of pg_kernels.cu; this file only allocates, launches, and reads
+// back the per-iteration switch counter (the loop's only device->host sync).
+#include <algorithm>
+#include <chrono>
+#include <climits>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "pg_internal.cuh"
+
+using namespace pgsi;
+
+static thread_local std::string t_err;
+
+static void set_err(const std::string &s) { t_err = s; }
+
+enum Phase { PH_V1 = 0, PH_V2, PH_ODD, PH_EVEN, PH_OTHER, PH_N };
+
+struct pg_game_s {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    uint32_t flags = 0;
+    int64_t max_inner = 0, max_outer = 0;
+    int64_t n = 0, m = 0, m_int = 0, dummies = 0, m_odd = 0;
+    std::vector<int32_t> D;
+    DevGame G{};
+    LaunchCfg lc;
+    int32_t *d_D = nullptr;
+    Ctl *h_ctl = nullptr;          // pinned readback
+    void *d_in = nullptr;          // staging (host-pointer mode)
+    size_t in_bytes = 0;
+    void *d_out = nullptr;
+    size_t out_bytes = 0;
+    std::vector<void *> allocs;
+    pg_stats st{};
+    bool broken = false;
+    // phase timing
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    struct Rec { int ph; cudaEvent_t a, b; };
+    std::vector<Rec> recs;
+};
+
+#define CK(h, x)                                                                         \
+    do {                                                                                 \
+        cudaError_t e_ = (x);                                                            \
+        if (e_ != cudaSuccess) {                                                         \
+            set_err(std::string(#x) + ": " + cudaGetErrorString(e_));                   \
+            if (h) (h)->broken = true;                                                   \
+            return PG_ECUDA;                                                             \
+        }                                                                                \
+    } while (0)
+
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+template <typename T>
+cudaError_t dalloc(pg_game h, T **p, size_t count) {
+    size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+    cudaError_t e = cudaMalloc((void **)p, bytes);
+    if (e == cudaSuccess) h->allocs.push_back((void *)*p);
+    return e;
+}
+
+void dfree(pg_game h, void *p) {
+    if (!p) return;
+    cudaFree(p);
+    h->allocs.erase(std::remove(h->allocs.begin(), h->allocs.end(), p), h->allocs.end());
+}
+
+cudaEvent_t ev_get(pg_game h) {
+    if (h->ev_used == h->ev_pool.size()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        h->ev_pool.push_back(e);
+    }
+    return h->ev_pool[h->ev_used++];
+}
+
+struct PhaseScope {
+    pg_game h;
+    int ph;
+    cudaEvent_t b = nullptr;
+    PhaseScope(pg_game h_, int ph_) : h(h_), ph(ph_) {
+        if (h->flags & PG_PHASE_TIMING) {
+            cudaEvent_t a = ev_get(h);
+            b = ev_get(h);
+            cudaEventRecord(a, h->stream);
+            h->recs.push_back({ph, a, b});
+        }
+    }
+    ~PhaseScope() {
+        if (b) cudaEventRecord(b, h->stream);
+    }
+};
+
+void timing_collect(pg_game h) {
+    for (auto &r : h->recs) {
+        float ms = 0;
+        if (cudaEventElapsedTime(&ms, r.a, r.b) != cudaSuccess) continue;
+        switch (r.ph) {
+            case PH_V1: h->st.ms_v1 += ms; h->st.n_v1++; break;
+            case PH_V2: h->st.ms_v2 += ms; h->st.n_v2++; break;
+            case PH_ODD: h->st.ms_odd += ms; h->st.n_odd++; break;
+            case PH_EVEN: h->st.ms_even += ms; h->st.n_even++; break;
+            default: h->st.ms_other += ms; break;
+        }
+    }
+    h->recs.clear();
+    h->ev_used = 0;
+}
+
+void reset_call_stats(pg_game h) {
+    pg_stats keep = h->st;
+    std::memset(&h->st, 0, sizeof(h->st));
+    h->st.n = keep.n;
+    h->st.n_internal = keep.n_internal;
+    h->st.m = keep.m;
+    h->st.m_internal = keep.m_internal;
+    h->st.d = keep.d;
+    h->st.dummies = keep.dummies;
+    h->st.ms_load = keep.ms_load;
+    h->recs.clear();
+    h->ev_used = 0;
+}
+
+pg_status grow_staging(pg_game h, void **buf, size_t *cap, size_t need) {
+    if (*cap >= need) return PG_OK;
+    if (*buf) dfree(h, *buf);
+    *buf = nullptr;
+    *cap = 0;
+    CK(h, cudaMalloc(buf, need));
+    h->allocs.push_back(*buf);
+    *cap = need;
+    return PG_OK;
+}
+
+pg_status grow_splitters(pg_game h, int64_t need) {
+    int64_t cap = std::min<int64_t>(h->G.n_int + 1, std::max<int64_t>(need + need / 4 + 1024, h->G.spl_cap * 2));
+    dfree(h, h->G.spl);
+    dfree(h, h->G.sJ[0]);
+    dfree(h, h->G.sJ[1]);
+    dfree(h, h->G.sacc[0]);
+    dfree(h, h->G.sacc[1]);
+    CK(h, dalloc(h, &h->G.spl, cap));
+    CK(h, dalloc(h, &h->G.sJ[0], cap));
+    CK(h, dalloc(h, &h->G.sJ[1], cap));
+    CK(h, dalloc(h, &h->G.sacc[0], (size_t)cap * h->G.dp));
+    CK(h, dalloc(h, &h->G.sacc[1], (size_t)cap * h->G.dp));
+    h->G.spl_cap = cap;
+    return PG_OK;
+}
+
+// One valuation of the current profile (σ ∪ τ in G.succ): V1 then V2.
+pg_status valuate_dev(pg_game h, bool want_cdom) {
+    if (want_cdom && !h->G.cJ[0]) {    // cycle-dominant scratch, allocated on first use
+        const size_t N1 = (size_t)h->G.n_int + 1;
+        CK(h, dalloc(h, &h->G.cJ[0], N1));
+        CK(h, dalloc(h, &h->G.cJ[1], N1));
+        CK(h, dalloc(h, &h->G.cmax[0], N1));
+        CK(h, dalloc(h, &h->G.cmax[1], N1));
+    }
+    CK(h, cudaMemsetAsync(h->G.ctl, 0, PGSI_CTL_RESET_BYTES, h->stream));
+    {
+        PhaseScope ps(h, PH_V1);
+        CK(h, launch_v1(h->G, h->lc, h->stream));
+        h->st.gpu_launches += 1;
+    }
+    {
+        PhaseScope ps(h, PH_V2);
+        int launches = 0;
+        CK(h, launch_splitters(h->G, h->lc, h->stream, &launches));
+        CK(h, launch_v2(h->G, h->stream));
+        h->st.gpu_launches += launches + 1;
+    }
+    if (want_cdom) {
+        PhaseScope ps(h, PH_OTHER);
+        CK(h, launch_cycle_dom(h->G, h->lc, h->stream));
+        h->st.gpu_launches += 1;
+    }
+    return PG_OK;
+}
+
+pg_status readback(pg_game h) {
+    CK(h, cudaMemcpyAsync(h->h_ctl, h->G.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    return PG_OK;
+}
+
+void note_valuation(pg_game h) {
+    const double np_ = (double)h->G.n_int, R = 4.0 * h->G.dp;
+    h->st.bytes_v1 += 5.0 * np_;
+    h->st.bytes_v2 += np_ + R * (double)h->h_ctl->n_fin;
+    h->st.v1_rounds += (int64_t)h->h_ctl->v1_rounds;
+    if ((int64_t)h->h_ctl->maxdepth > h->st.max_depth) h->st.max_depth = (int64_t)h->h_ctl->maxdepth;
+    if ((int64_t)h->h_ctl->maxdepth >= h->G.K) h->st.v2_split_valuations++;
+}
+
+// valuation + one switch step, redone if the splitter buffers overflowed.
+pg_status valuate_and_switch(pg_game h, bool odd, bool want_cdom, bool do_switch) {
+    for (;;) {
+        pg_status rc = valuate_dev(h, want_cdom);
+        if (rc) return rc;
+        if (do_switch) {
+            PhaseScope ps(h, odd ? PH_ODD : PH_EVEN);
+            CK(h, launch_switch(h->G, odd, h->stream));
+            h->st.gpu_launches += 1;
+        }
+        rc = readback(h);
+        if (rc) return rc;
+        if (!h->h_ctl->spl_overflow) break;
+        rc = grow_splitters(h, (int64_t)h->h_ctl->nspl);   // rare: redo with larger buffers
+        if (rc) return rc;
+    }
+    note_valuation(h);
+    return PG_OK;
+}
+
+// Inner loop of Algorithm 1: valuate, All_Odd, until S_Odd = ∅.
+pg_status inner_loop(pg_game h, int64_t *inner, bool check) {
+    for (;;) {
+        if (h->max_inner > 0 && *inner >= h->max_inner) {
+            set_err("inner iteration cap reached");
+            return PG_EITERCAP;
+        }
+        pg_status rc = valuate_and_switch(h, true, check, true);
+        if (rc) return rc;
+        (*inner)++;
+        if (check && h->h_ctl->odd_cycle) {
+            set_err("odd cycle reached: strategy not admissible");
+            return PG_EINADMISSIBLE;
+        }
+        int64_t c = (int64_t)h->h_ctl->odd_switches;
+        h->st.odd_switches += c;
+        {
+            const double no = (double)(h->G.n_int - h->G.n_even), mo = (double)h->m_odd;
+            h->st.bytes_odd += 4.0 * (no + 1) + 4.0 * no + 5.0 * mo + no +
+                               4.0 * h->G.dp * (double)h->h_ctl->rows_odd + 4.0 * c;
+        }
+        if (c == 0) return PG_OK;
+    }
+}
+
+pg_status even_switch(pg_game h, int64_t *count) {
+    CK(h, cudaMemsetAsync(&h->G.ctl->even_switches, 0, sizeof(unsigned long long), h->stream));
+    CK(h, cudaMemsetAsync(&h->G.ctl->rows_even, 0, sizeof(unsigned long long), h->stream));
+    {
+        PhaseScope ps(h, PH_EVEN);
+        CK(h, launch_switch(h->G, false, h->stream));
+        h->st.gpu_launches += 1;
+    }
+    pg_status rc = readback(h);
+    if (rc) return rc;
+    *count = (int64_t)h->h_ctl->even_switches;
+    h->st.even_switches += *count;
+    {
+        const double ne = (double)h->G.n_even, me = (double)(h->m_int - h->m_odd);
+        h->st.bytes_even += 4.0 * (ne + 1) + 4.0 * ne + 5.0 * me + ne +
+                            4.0 * h->G.dp * (double)h->h_ctl->rows_even + 4.0 * *count;
+    }
+    return PG_OK;
+}
+
+pg_status import_strategy(pg_game h, const int32_t *abi, int mode) {
+    const int32_t *src = abi;
+    if (!(h->flags & PG_PTRS_ON_DEVICE)) {
+        size_t bytes = sizeof(int32_t) * (size_t)h->G.n_int;
+        pg_status rc = grow_staging(h, &h->d_in, &h->in_bytes, bytes);
+        if (rc) return rc;
+        CK(h, cudaMemcpyAsync(h->d_in, abi, bytes, cudaMemcpyHostToDevice, h->stream));
+        src = (const int32_t *)h->d_in;
+    }
+    unsigned long long none = ULLONG_MAX;
+    CK(h, cudaMemcpyAsync(&h->G.ctl->bad_index, &none, sizeof(none), cudaMemcpyHostToDevice, h->stream));
+    CK(h, launch_import_strategy(h->G, src, mode, h->stream));
+    h->st.gpu_launches += 1;
+    pg_status rc = readback(h);
+    if (rc) return rc;
+    if (h->h_ctl->bad_index != ULLONG_MAX) {
+        set_err("strategy entry at vertex " + std::to_string(h->h_ctl->bad_index) + " is not an edge");
+        return PG_EINVAL;
+    }
+    return PG_OK;
+}
+
+// Output helper: device-pointer mode writes straight into the caller's buffer,
+// host mode stages on the device and copies back.
+struct OutBuf {
+    void *user;
+    void *dev;
+    size_t bytes;
+};
+
+pg_status outputs_begin(pg_game h, std::vector<OutBuf> &outs) {
+    if (h->flags & PG_PTRS_ON_DEVICE) {
+        for (auto &o : outs) o.dev = o.user;
+        return PG_OK;
+    }
+    size_t total = 0;
+    for (auto &o : outs) if (o.user) total += (o.bytes + 255) & ~size_t(255);
+    pg_status rc = grow_staging(h, &h->d_out, &h->out_bytes, total);
+    if (rc) return rc;
+    size_t off = 0;
+    for (auto &o : outs) {
+        o.dev = nullptr;
+        if (!o.user) continue;
+        o.dev = (char *)h->d_out + off;
+        off += (o.bytes + 255) & ~size_t(255);
+    }
+    return PG_OK;
+}
+
+pg_status outputs_end(pg_game h, std::vector<OutBuf> &outs) {
+    if (!(h->flags & PG_PTRS_ON_DEVICE))
+        for (auto &o : outs)
+            if (o.user && o.bytes)
+                CK(h, cudaMemcpyAsync(o.user, o.dev, o.bytes, cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    return PG_OK;
+}
+
+double now_ms() {
+    using namespace std::chrono;
+    return duration<double, std::milli>(steady_clock::now().time_since_epoch()).count();
+}
+
+pg_status check_handle(pg_game h) {
+    if (!h) { set_err("NULL handle"); return PG_EINVAL; }
+    if (h->broken) { set_err("handle unusable after an earlier CUDA error"); return PG_ESTATE; }
+    return PG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *pg_last_error(void) { return t_err.c_str(); }
+
+const char *pg_version(void) { return "pgsi-b200 0.1 (sm_100a)"; }
+
+void pg_free(pg_game h) {
+    if (!h) return;
+    DeviceGuard dg(h->device);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    for (void *p : h->allocs) cudaFree(p);
+    if (h->h_ctl) cudaFreeHost(h->h_ctl);
+    for (auto e : h->ev_pool) cudaEventDestroy(e);
+    if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+    delete h;
+}
+
+pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const uint8_t *owner,
+                  const int32_t *priority, const pg_options *opt, pg_game *out) {
+    if (!out) { set_err("NULL out"); return PG_EINVAL; }
+    *out = nullptr;
+    double t0 = now_ms();
+    pg_options o{};
+    if (opt) o = *opt;
+    HostGame H;
+    std::string err;
+    pg_status rc = build_host_game(n, row_ptr, col, owner, priority, !(o.flags & PG_NO_PREPROCESS), H, err);
+    if (rc) { set_err(err); return rc; }
+
+    pg_game h = new pg_game_s();
+    h->device = o.device;
+    h->flags = o.flags;
+    h->max_inner = o.max_inner;
+    h->max_outer = o.max_outer;
+    h->n = H.n;
+    h->m = H.m;
+    h->m_int = H.m_int;
+    h->dummies = H.dummies;
+    h->D = H.D;
+    h->m_odd = (int64_t)H.m_int - (int64_t)H.rp[H.n_even];
+    DeviceGuard dg(h->device);
+    auto fail = [&](pg_status r) { pg_free(h); return r; };
+#define CKL(x)                                                                  \
+    do {                                                                        \
+        cudaError_t e_ = (x);                                                   \
+        if (e_ != cudaSuccess) {                                                \
+            set_err(std::string(#x) + ": " + cudaGetErrorString(e_));          \
+            return fail(e_ == cudaErrorMemoryAllocation ? PG_ENOMEM : PG_ECUDA); \
+        }                                                                       \
+    } while (0)
+    CKL(cudaSetDevice(h->device));
+    if (o.stream) {
+        h->stream = (cudaStream_t)o.stream;
+    } else {
+        CKL(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        h->own_stream = true;
+    }
+    CKL(setup_launch_cfg(h->lc, h->device));
+
+    DevGame &G = h->G;
+    G.n_int = H.n_int;
+    G.n_even = H.n_even;
+    G.d = H.d;
+    int dp = 1;                          // row width: pow2 up to 128, else multiple of 32
+    if (H.d <= 128) { while (dp < H.d) dp <<= 1; }
+    else dp = (H.d + 31) / 32 * 32;
+    G.dp = dp;
+    G.K = o.splitter_k > 0 ? std::min(o.splitter_k, 255) : 32;
+    const size_t N1 = (size_t)H.n_int + 1;
+    uint32_t *rp; int32_t *colp; uint8_t *pidx, *oddp;
+    int32_t *perm, *iperm, *proj;
+    CKL(dalloc(h, &rp, N1));
+    CKL(dalloc(h, &colp, (size_t)H.m_int));
+    CKL(dalloc(h, &pidx, N1));
+    CKL(dalloc(h, &oddp, (size_t)std::max(dp, 32)));
+    CKL(dalloc(h, &G.succ, N1));
+    CKL(dalloc(h, &G.jl, N1));
+    CKL(dalloc(h, &G.top, N1));
+    CKL(dalloc(h, &G.val, N1 * dp));
+    CKL(dalloc(h, &G.sidx, N1));
+    CKL(dalloc(h, &perm, (size_t)H.n_int));
+    CKL(dalloc(h, &iperm, (size_t)H.n_int));
+    CKL(dalloc(h, &proj, (size_t)H.n_int));
+    CKL(dalloc(h, &G.ctl, 1));
+    CKL(dalloc(h, &h->d_D, (size_t)std::max(1, H.d)));
+    CKL(cudaMallocHost((void **)&h->h_ctl, sizeof(Ctl)));
+    G.rp = rp; G.col = colp; G.pidx = pidx; G.oddp = oddp;
+    G.perm = perm; G.iperm = iperm; G.proj = proj;
+    std::vector<uint8_t> odd(std::max(dp, 32), 0);
+    for (int i = 0; i < H.d; i++) odd[i] = (uint8_t)(H.D[i] & 1);
+    cudaStream_t s = h->stream;
+    CKL(cudaMemcpyAsync(rp, H.rp.data(), sizeof(uint32_t) * N1, cudaMemcpyHostToDevice, s));
+    if (H.m_int) CKL(cudaMemcpyAsync(colp, H.col.data(), sizeof(int32_t) * H.m_int, cudaMemcpyHostToDevice, s));
+    CKL(cudaMemcpyAsync(pidx, H.pidx.data(), N1, cudaMemcpyHostToDevice, s));
+    CKL(cudaMemcpyAsync(oddp, odd.data(), odd.size(), cudaMemcpyHostToDevice, s));
+    if (H.n_int) {
+        CKL(cudaMemcpyAsync(perm, H.perm.data(), sizeof(int32_t) * H.n_int, cudaMemcpyHostToDevice, s));
+        CKL(cudaMemcpyAsync(iperm, H.iperm.data(), sizeof(int32_t) * H.n_int, cudaMemcpyHostToDevice, s));
+        CKL(cudaMemcpyAsync(proj, H.proj.data(), sizeof(int32_t) * H.n_int, cudaMemcpyHostToDevice, s));
+    }
+    if (H.d) CKL(cudaMemcpyAsync(h->d_D, H.D.data(), sizeof(int32_t) * H.d, cudaMemcpyHostToDevice, s));
+    CKL(cudaMemsetAsync(G.val, 0, sizeof(int32_t) * N1 * dp, s));   // sink row = 0
+    CKL(cudaMemsetAsync(G.top, 0, N1, s));
+    CKL(cudaMemsetAsync(G.ctl, 0, sizeof(Ctl), s));
+    // splitter buffers: grown on demand (overflow protocol in valuate_and_switch)
+    {
+        int64_t cap = std::min<int64_t>(H.n_int + 1, H.n_int / G.K + 4096);
+        CKL(dalloc(h, &G.spl, (size_t)cap));
+        CKL(dalloc(h, &G.sJ[0], (size_t)cap));
+        CKL(dalloc(h, &G.sJ[1], (size_t)cap));
+        CKL(dalloc(h, &G.sacc[0], (size_t)cap * dp));
+        CKL(dalloc(h, &G.sacc[1], (size_t)cap * dp));
+        G.spl_cap = cap;
+    }
+    CKL(launch_init_profile(G, s));
+    CKL(cudaStreamSynchronize(s));
+#undef CKL
+    h->st.n = H.n;
+    h->st.n_internal = H.n_int;
+    h->st.m = H.m;
+    h->st.m_internal = H.m_int;
+    h->st.d = H.d;
+    h->st.dummies = H.dummies;
+    h->st.ms_load = now_ms() - t0;
+    *out = h;
+    return PG_OK;
+}
+
+pg_status pg_info(pg_game h, int64_t *n_internal, int32_t *d, int32_t *priorities, int64_t *dummies) {
+    if (!h) { set_err("NULL handle"); return PG_EINVAL; }
+    if (n_internal) *n_internal = h->G.n_int;
+    if (d) *d = (int32_t)h->D.size();
+    if (priorities) std::memcpy(priorities, h->D.data(), sizeof(int32_t) * h->D.size());
+    if (dummies) *dummies = h->dummies;
+    return PG_OK;
+}
+
+pg_status pg_inspect(int64_t n, const int64_t *row_ptr, const int32_t *col, const uint8_t *owner,
+                     const int32_t *priority, uint32_t flags, int64_t *n_internal, int32_t *d,
+                     int64_t *dummies, int64_t *m_internal, uint8_t *owner_int, int32_t *pidx_int,
+                     int64_t *adj_ptr, int32_t *adj, int32_t *priorities) {
+    HostGame H;
+    std::string err;
+    pg_status rc = build_host_game(n, row_ptr, col, owner, priority, !(flags & PG_NO_PREPROCESS), H, err);
+    if (rc) { set_err(err); return rc; }
+    if (n_internal) *n_internal = H.n_int;
+    if (d) *d = H.d;
+    if (dummies) *dummies = H.dummies;
+    if (m_internal) *m_internal = H.m_int;
+    if (priorities) std::memcpy(priorities, H.D.data(), sizeof(int32_t) * H.D.size());
+    int64_t o = 0;
+    for (int64_t a = 0; a < H.n_int; a++) {
+        int32_t v = H.perm[a];
+        if (owner_int) owner_int[a] = v < H.n_even ? 0 : 1;
+        if (pidx_int) pidx_int[a] = H.pidx[v];
+        if (adj_ptr) adj_ptr[a] = o;
+        for (uint32_t e = H.rp[v]; e < H.rp[v + 1]; e++) {
+            if (adj) adj[o] = H.iperm[H.col[e]];
+            o++;
+        }
+    }
+    if (adj_ptr) adj_ptr[H.n_int] = o;
+    return PG_OK;
+}
+
+pg_status pg_get_stats(pg_game h, pg_stats *stats) {
+    if (!h || !stats) { set_err("NULL argument"); return PG_EINVAL; }
+    *stats = h->st;
+    return PG_OK;
+}
+
+pg_status pg_valuate(pg_game h, const int32_t *strategy, int32_t *val, uint8_t *top, int32_t *cycle_dom) {
+    pg_status rc = check_handle(h);
+    if (rc) return rc;
+    if (!strategy && h->G.n_int) { set_err("NULL strategy"); return PG_EINVAL; }
+    DeviceGuard dg(h->device);
+    reset_call_stats(h);
+    double t0 = now_ms();
+    if (h->G.n_int == 0) return PG_OK;
+    if ((rc = import_strategy(h, strategy, 3))) return rc;
+    if ((rc = valuate_and_switch(h, true, cycle_dom != nullptr, false))) return rc;
+    h->st.inner_iters = 1;
+    const int64_t N = h->G.n_int;
+    std::vector<OutBuf> outs = {{val, nullptr, sizeof(int32_t) * (size_t)N * h->D.size()},
+                                {top, nullptr, (size_t)N},
+                                {cycle_dom, nullptr, sizeof(int32_t) * (size_t)N}};
+    if ((rc = outputs_begin(h, outs))) return rc;
+    if (val || top) CK(h, launch_export_val(h->G, N, (int32_t *)outs[0].dev, (uint8_t *)outs[1].dev, h->stream));
+    if (cycle_dom) CK(h, launch_export_cycle_dom(h->G, N, h->d_D, (int32_t *)outs[2].dev, h->stream));
+    if ((rc = outputs_end(h, outs))) return rc;
+    timing_collect(h);
+    h->st.ms_call = now_ms() - t0;
+    return PG_OK;
+}
+
+pg_status pg_best_response(pg_game h, const int32_t *sigma, const int32_t *tau0, int32_t *tau_out,
+                           int32_t *val, uint8_t *top, int64_t *inner_iters) {
+    pg_status rc = check_handle(h);
+    if (rc) return rc;
+    if (!sigma && h->G.n_int) { set_err("NULL sigma"); return PG_EINVAL; }
+    DeviceGuard dg(h->device);
+    reset_call_stats(h);
+    double t0 = now_ms();
+    int64_t inner = 0;
+    const int64_t N = h->G.n_int;
+    if (N) {
+        if ((rc = import_strategy(h, sigma, tau0 ? 1 : 1 | 4))) return rc;
+        if (tau0 && (rc = import_strategy(h, tau0, 2))) return rc;
+        rc = inner_loop(h, &inner, true);   // arbitrary σ: always check admissibility
+        if (inner_iters) *inner_iters = inner;
+        h->st.inner_iters = inner;
+        if (rc) return rc;
+    } else if (inner_iters) {
+        *inner_iters = 0;
+    }
+    std::vector<OutBuf> outs = {{tau_out, nullptr, sizeof(int32_t) * (size_t)N},
+                                {val, nullptr, sizeof(int32_t) * (size_t)N * h->D.size()},
+                                {top, nullptr, (size_t)N}};
+    if ((rc = outputs_begin(h, outs))) return rc;
+    if (N && tau_out) CK(h, launch_export_strategy(h->G, N, (int32_t *)outs[0].dev, 1, false, h->stream));
+    if (N && (val || top)) CK(h, launch_export_val(h->G, N, (int32_t *)outs[1].dev, (uint8_t *)outs[2].dev, h->stream));
+    if ((rc = outputs_end(h, outs))) return rc;
+    timing_collect(h);
+    h->st.ms_call = now_ms() - t0;
+    return PG_OK;
+}
+
+pg_status pg_solve(pg_game h, uint8_t *winner, int32_t *sigma, int32_t *tau, int32_t *val, pg_stats *stats) {
+    pg_status rc = check_handle(h);
+    if (rc) return rc;
+    if (!winner && h->n) { set_err("NULL winner"); return PG_EINVAL; }
+    DeviceGuard dg(h->device);
+    reset_call_stats(h);
+    double t0 = now_ms();
+    int64_t inner = 0, outer = 0;
+    // With preprocessing σ_init is admissible and Thm 2 keeps every σ admissible
+    // (PAPER.md:436-443), so odd cycles are only checked on request / without it.
+    const bool check = (h->flags & (PG_CHECK_INVARIANTS | PG_NO_PREPROCESS)) != 0;
+    if (h->G.n_int) {
+        {
+            PhaseScope ps(h, PH_OTHER);
+            CK(h, launch_init_profile(h->G, h->stream));   // σ_init, τ = first successor
+            h->st.gpu_launches += 1;
+        }
+        for (;;) {                                           // Algorithm 1, outer repeat
+            if (h->max_outer > 0 && outer >= h->max_outer) {
+                set_err("outer pass cap reached");
+                rc = PG_EITERCAP;
+                break;
+            }
+            rc = inner_loop(h, &inner, check);               // τ := br(σ), warm-started
+            if (rc) break;
+            outer++;
+            int64_t c = 0;
+            rc = even_switch(h, &c);                         // σ := σ[All_Even(σ)]
+            if (rc || c == 0) break;                         // until S_Even = ∅
+        }
+    }
+    h->st.inner_iters = inner;
+    h->st.outer_passes = outer;
+    if (rc) { timing_collect(h); if (stats) *stats = h->st; return rc; }
+    const int64_t n = h->n;
+    std::vector<OutBuf> outs = {{winner, nullptr, (size_t)n},
+                                {sigma, nullptr, sizeof(int32_t) * (size_t)n},
+                                {tau, nullptr, sizeof(int32_t) * (size_t)n},
+                                {val, nullptr, sizeof(int32_t) * (size_t)n * h->D.size()}};
+    if ((rc = outputs_begin(h, outs))) return rc;
+    if (n) {
+        PhaseScope ps(h, PH_OTHER);
+        CK(h, launch_export_winner(h->G, n, (uint8_t *)outs[0].dev, h->stream));
+        h->st.gpu_launches += 1;
+        if (sigma) { CK(h, launch_export_strategy(h->G, n, (int32_t *)outs[1].dev, 0, false, h->stream)); h->st.gpu_launches++; }
+        if (tau) { CK(h, launch_export_strategy(h->G, n, (int32_t *)outs[2].dev, 1, true, h->stream)); h->st.gpu_launches++; }
+        if (val) { CK(h, launch_export_val(h->G, n, (int32_t *)outs[3].dev, nullptr, h->stream)); h->st.gpu_launches++; }
+    }
+    if ((rc = outputs_end(h, outs))) return rc;
+    timing_collect(h);
+    h->st.ms_call = now_ms() - t0;
+    if (stats) *stats = h->st;
+    return PG_OK;
+}
+
+}  // extern "C"

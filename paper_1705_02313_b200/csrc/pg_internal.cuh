@@ -1,0 +1,122 @@
+// pg_internal.cuh — private declarations shared by the host side (pg_load.cpp,
+// pg_api.cu) and the kernels (pg_kernels.cu) of libpgsi.so.
+//
+// Device-side game layout:
+//   * device vertex order: [Even originals | dummies | Odd originals], each in
+//     ABI order, so All_Even / All_Odd run over plain index ranges;
+//     SINK = n_int is a real row (zero valuation, never ⊤);
+//   * rp  : uint32[n_int+1]   CSR offsets (canonical order: ascending original id,
+//           dummy w_v at v's position; the sink candidate of Even vertices is
+//           implicit and ordered last, SURVEY.md §8(c) reading 3);
+//   * col : int32[m_int]      successor device ids;
+//   * pidx: uint8[n_int+1]    index of pri(v) in D (d <= 256);
+//   * succ: int32[n_int+1]    current profile σ ∪ τ (succ[SINK] = SINK);
+//   * jl  : u64[n_int+1]      V1 pointer-jumping state (J | len << 32);
+//   * top : uint8[n_int+1]    1 iff val(v) = ⊤;
+//   * val : int32[(n_int+1)*dp] sign-adjusted keys k_i = sgn(D[i])·count_i
+//           (sgn = -1 for odd D[i]) so that ⊑ is plain lexicographic order on keys
+//           from the highest column down.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+#include <string>
+#include <vector>
+
+#include "pg.h"
+
+namespace pgsi {
+
+constexpr int kMaxD = 256;       // pidx is uint8
+constexpr int kThreads = 256;
+
+// Per-valuation / per-call device counters (one block of device memory).
+struct Ctl {
+    unsigned long long newfin[3];   // V1: vertices newly reaching the sink per round (rotating)
+    unsigned long long v1_rounds;   // V1 rounds in the last valuation
+    unsigned long long maxdepth;    // deepest finite play of the last valuation
+    unsigned long long nspl;        // splitters of the last valuation
+    unsigned long long spl_active[3];
+    unsigned long long spl_final;   // which Sacc buffer holds the final rows
+    unsigned long long odd_cycle;   // set if a reached cycle has an odd dominant priority
+    unsigned long long spl_overflow;// splitter count exceeded the splitter buffers' capacity
+    unsigned long long odd_switches;
+    unsigned long long even_switches;
+    unsigned long long cdom_buf;    // which cJ buffer holds cycle_dom (pidx or -1)
+    unsigned long long n_fin;       // finite vertices of the last valuation
+    unsigned long long rows_odd;    // rows gathered by the last All_Odd launch
+    unsigned long long rows_even;   // rows gathered by the last All_Even launch
+    // ---- not reset per valuation ----
+    unsigned long long bad_index;   // ULLONG_MAX = none, else min invalid ABI index
+    unsigned int bar_count;         // grid barrier
+    unsigned int bar_gen;
+};
+#define PGSI_CTL_RESET_BYTES offsetof(pgsi::Ctl, bad_index)
+
+struct DevGame {
+    int64_t n_int;      // internal vertices; SINK = n_int
+    int64_t n_even;     // device ids [0, n_even) are Even
+    int32_t d;          // |D|
+    int32_t dp;         // padded row width (pow2 <= 128, else multiple of 32)
+    int32_t K;          // splitter depth stride
+    int64_t spl_cap;    // capacity of spl / sJ / sacc (rows)
+    const uint32_t *rp;
+    const int32_t *col;
+    const uint8_t *pidx;
+    const uint8_t *oddp; // oddp[i] = D[i] is odd (dp entries, padding = 0)
+    int32_t *succ;
+    unsigned long long *jl;
+    uint8_t *top;
+    int32_t *val;
+    int32_t *sidx;
+    int32_t *spl;
+    int32_t *sJ[2];
+    int32_t *sacc[2];
+    int32_t *cmax[2];   // cycle-dominant pointer jumping (pg_valuate)
+    int32_t *cJ[2];
+    const int32_t *perm;   // ABI -> device
+    const int32_t *iperm;  // device -> ABI
+    const int32_t *proj;   // device -> ABI id with dummies projected to their vertex
+    Ctl *ctl;
+};
+
+struct LaunchCfg {
+    int sms = 148;
+    int coop_v1 = 0;        // cooperative grid sizes
+    int coop_spl = 0;
+    int coop_cyc = 0;
+};
+
+// kernels (pg_kernels.cu); every launcher returns the cudaError_t of the launch
+cudaError_t launch_init_profile(const DevGame &g, cudaStream_t s);
+cudaError_t launch_import_strategy(const DevGame &g, const int32_t *abi_strategy, int mode,
+                                   cudaStream_t s);
+cudaError_t launch_v1(const DevGame &g, const LaunchCfg &lc, cudaStream_t s);
+cudaError_t launch_splitters(const DevGame &g, const LaunchCfg &lc, cudaStream_t s, int *launches);
+cudaError_t launch_v2(const DevGame &g, cudaStream_t s);
+cudaError_t launch_cycle_dom(const DevGame &g, const LaunchCfg &lc, cudaStream_t s);
+cudaError_t launch_switch(const DevGame &g, bool odd, cudaStream_t s);
+cudaError_t launch_export_val(const DevGame &g, int64_t count, int32_t *val_out, uint8_t *top_out,
+                              cudaStream_t s);
+cudaError_t launch_export_strategy(const DevGame &g, int64_t count, int32_t *out, int which,
+                                   bool project, cudaStream_t s);
+cudaError_t launch_export_winner(const DevGame &g, int64_t count, uint8_t *out, cudaStream_t s);
+cudaError_t launch_export_cycle_dom(const DevGame &g, int64_t count, const int32_t *D_dev,
+                                    int32_t *out, cudaStream_t s);
+cudaError_t setup_launch_cfg(LaunchCfg &lc, int device);
+
+// host-side canonical game (pg_load.cpp)
+struct HostGame {
+    int64_t n = 0, m = 0, n_int = 0, m_int = 0, dummies = 0, n_even = 0;
+    int32_t d = 0;
+    std::vector<int32_t> D;
+    std::vector<int32_t> perm, iperm, proj;   // proj: device -> projected ABI id
+    std::vector<uint32_t> rp;                 // device order
+    std::vector<int32_t> col;
+    std::vector<uint8_t> pidx;
+};
+pg_status build_host_game(int64_t n, const int64_t *row_ptr, const int32_t *col,
+                          const uint8_t *owner, const int32_t *priority, bool preprocess,
+                          HostGame &out, std::string &err);
+
+}  // namespace pgsi

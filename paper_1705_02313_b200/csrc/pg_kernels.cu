@@ -1,0 +1,835 @@
+// pg_kernels.cu — sm_100a kernels of the valuation + all-switches hot path.
+//
+// Hot path per inner iteration of Algorithm 1:
+//   V1  k_v1            sink reachability / ⊤ detection / depth by in-place pointer
+//                       jumping on packed (J, len) words
+//   V2  k_spl_*         (only when some play is deeper than K) depth-strided
+//                       splitters + Wyllie over the reduced forest's d-vector rows
+//       k_v2_walk       d-vector path counts: each lane walks its
+//                       vertex's play to the sink or the nearest splitter with a
+//                       byte-packed register histogram, then the warp writes the
+//                       32 rows as coalesced row stores (the list-ranking step of
+//                       PAPER.md:613-653, re-designed)
+//   S   k_switch<ODD>   All_Odd / All_Even
+//                       (PAPER.md:416-434, 487-491): a group of dp lanes per vertex,
+//                       one key column per lane, lexicographic compare by two warp
+//                       ballots; switch counts by ballot+popc, one atomic per block
+//                       (convergence test, Algorithm 1 "until S = ∅").
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "pg_internal.cuh"
+
+namespace pgsi {
+
+#define FULL 0xffffffffu
+
+__device__ __forceinline__ unsigned long long ldcg64(const unsigned long long *p) {
+    return __ldcg(p);
+}
+__device__ __forceinline__ unsigned long long pack_jl(uint32_t J, uint32_t len) {
+    return (unsigned long long)J | ((unsigned long long)len << 32);
+}
+
+// Software grid barrier for cooperative (co-resident) launches.
+__device__ __forceinline__ void grid_barrier(Ctl *ctl) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned *genp = &ctl->bar_gen;
+        unsigned gen = *genp;
+        __threadfence();
+        unsigned arrived = atomicAdd(&ctl->bar_count, 1u);
+        if (arrived == gridDim.x - 1) {
+            ctl->bar_count = 0;
+            __threadfence();
+            atomicAdd(&ctl->bar_gen, 1u);
+        } else {
+            while (*genp == gen) __nanosleep(20);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+template <typename T>
+__device__ __forceinline__ T block_sum(T x) {
+    __shared__ T red[32];
+    for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(FULL, x, o);
+    int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) red[w] = x;
+    __syncthreads();
+    T s = 0;
+    if (threadIdx.x == 0)
+        for (int i = 0; i < (int)(blockDim.x >> 5); i++) s += red[i];
+    return s;  // valid in thread 0
+}
+
+template <typename T>
+__device__ __forceinline__ T block_max(T x) {
+    __shared__ T red[32];
+    for (int o = 16; o; o >>= 1) { T y = __shfl_xor_sync(FULL, x, o); x = y > x ? y : x; }
+    int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) red[w] = x;
+    __syncthreads();
+    T s = 0;
+    if (threadIdx.x == 0)
+        for (int i = 0; i < (int)(blockDim.x >> 5); i++) s = red[i] > s ? red[i] : s;
+    return s;
+}
+
+// --------------------------------------------------------------------------
+// profile init / import
+// --------------------------------------------------------------------------
+__global__ void k_init_profile(DevGame g) {
+    // σ_init(v) = s for Even; τ(v) = first successor (reading 4)
+    int64_t N = g.n_int;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v <= N;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        int32_t s;
+        if (v == N || v < g.n_even) s = (int32_t)N;
+        else s = g.col[g.rp[v]];
+        g.succ[v] = s;
+    }
+}
+
+// mode bit0: Even entries from the array (else σ kept), bit1: Odd entries from the
+// array (else τ = first successor when bit2, else kept). Validates edges.
+__global__ void k_import_strategy(DevGame g, const int32_t *abi, int mode) {
+    int64_t N = g.n_int;
+    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < N;
+         a += (int64_t)gridDim.x * blockDim.x) {
+        int32_t v = g.perm[a];
+        bool even = v < g.n_even;
+        uint32_t b = g.rp[v], e = g.rp[v + 1];
+        int32_t s;
+        if (even) {
+            if (!(mode & 1)) continue;
+            int32_t x = abi[a];
+            if (x == PG_SINK) { g.succ[v] = (int32_t)N; continue; }
+            if (x < 0 || x >= N) { atomicMin(&g.ctl->bad_index, (unsigned long long)a); continue; }
+            s = g.perm[x];
+        } else {
+            if (!(mode & 2)) {
+                if (mode & 4) g.succ[v] = g.col[b];
+                continue;
+            }
+            int32_t x = abi[a];
+            if (x < 0 || x >= N) { atomicMin(&g.ctl->bad_index, (unsigned long long)a); continue; }
+            s = g.perm[x];
+        }
+        bool ok = false;
+        for (uint32_t k = b; k < e; k++) ok |= g.col[k] == s;
+        if (!ok) { atomicMin(&g.ctl->bad_index, (unsigned long long)a); continue; }
+        g.succ[v] = s;
+    }
+}
+
+// --------------------------------------------------------------------------
+// V1: in-place pointer jumping on (J, len). Stop after the first round in which
+// no vertex newly reaches the sink (DESIGN.md §V1 proves this is exact). ⊤ =
+// vertices whose J never reaches the sink.
+// --------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_v1(DevGame g) {
+    const int64_t N = g.n_int;
+    const uint32_t SINK = (uint32_t)N;
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    unsigned long long *jl = g.jl;
+    for (int64_t v = tid; v < N; v += stride)
+        jl[v] = pack_jl((uint32_t)__ldg(g.succ + v), 1u);
+    grid_barrier(g.ctl);
+    int r = 0;
+    for (;;) {
+        unsigned long long local = 0;
+        for (int64_t v = tid; v < N; v += stride) {
+            unsigned long long e = ldcg64(jl + v);
+            uint32_t J = (uint32_t)e;
+            if (J == SINK) continue;
+            unsigned long long f = ldcg64(jl + J);
+            uint32_t nJ = (uint32_t)f;
+            uint32_t s = (uint32_t)(e >> 32) + (uint32_t)(f >> 32);
+            if (s > 0x7fffffffu) s = 0x7fffffffu;   // only ⊤ vertices can saturate
+            __stcg(jl + v, pack_jl(nJ, s));
+            local += (nJ == SINK);
+        }
+        unsigned long long tot = block_sum(local);
+        if (threadIdx.x == 0 && tot) atomicAdd(&g.ctl->newfin[r % 3], tot);
+        grid_barrier(g.ctl);
+        unsigned long long nf = *(volatile unsigned long long *)&g.ctl->newfin[r % 3];
+        if (blockIdx.x == 0 && threadIdx.x == 0) g.ctl->newfin[(r + 2) % 3] = 0;
+        r++;
+        if (nf == 0) break;
+    }
+    unsigned long long mx = 0, nf = 0;
+    for (int64_t v = tid; v < N; v += stride) {
+        unsigned long long e = ldcg64(jl + v);
+        bool fin = (uint32_t)e == SINK;
+        g.top[v] = fin ? 0 : 1;
+        if (fin) { unsigned long long dd = e >> 32; mx = dd > mx ? dd : mx; nf++; }
+    }
+    mx = block_max(mx);
+    if (threadIdx.x == 0 && mx) atomicMax(&g.ctl->maxdepth, mx);
+    nf = block_sum(nf);
+    if (threadIdx.x == 0 && nf) atomicAdd(&g.ctl->n_fin, nf);
+    if (blockIdx.x == 0 && threadIdx.x == 0) { g.ctl->v1_rounds = r; g.top[N] = 0; }
+}
+
+// --------------------------------------------------------------------------
+// V2 helpers: byte-packed per-lane histogram of priorities met along a walk.
+// --------------------------------------------------------------------------
+template <int NW>
+__device__ __forceinline__ void hist_add(uint32_t (&h)[NW], uint32_t p) {
+    uint32_t inc = 1u << ((p & 3u) * 8u);
+    uint32_t w = p >> 2;
+#pragma unroll
+    for (int q = 0; q < NW; q++) h[q] += (w == (uint32_t)q) ? inc : 0u;
+}
+
+// Walk `steps` successors from x, counting priorities in [lo, lo + 4*NW).
+template <int NW>
+__device__ __forceinline__ int32_t walk(const DevGame &g, int32_t x, uint32_t steps, uint32_t lo,
+                                        uint32_t (&h)[NW]) {
+    for (uint32_t s = 0; s < steps; s++) {
+        uint32_t p = (uint32_t)__ldg(g.pidx + x) - lo;
+        int32_t nx = __ldg(g.succ + x);
+        if (p < 4u * NW) hist_add<NW>(h, p);
+        x = nx;
+    }
+    return x;
+}
+
+// Warp-cooperative row output: lane l holds a histogram for slot l (packed as
+// 8 words of 4 byte-counts). Rows are written by groups of GW = cols/VEC lanes,
+// each lane storing VEC consecutive key columns (one histogram word when VEC =
+// 4) with a single vector store; key = sgn·count (+ the base row from `sacc`
+// when base >= 0). cols = columns covered per chunk (min(dp, 32)).
+template <int VEC>
+__device__ __forceinline__ void store_vec(int32_t *p, const int32_t (&r)[VEC]) {
+    if constexpr (VEC == 4) *reinterpret_cast<int4 *>(p) = make_int4(r[0], r[1], r[2], r[3]);
+    else if constexpr (VEC == 2) *reinterpret_cast<int2 *>(p) = make_int2(r[0], r[1]);
+    else *p = r[0];
+}
+
+template <int GW, int VEC>
+__device__ __forceinline__ void write_rows(uint32_t (*hs)[9], const int32_t *bases,
+                                           const int64_t *rowid, int32_t *out, int dp,
+                                           int col0, const int32_t *sacc, const uint8_t *oddp) {
+    const int lane = threadIdx.x & 31;
+    constexpr int R = 32 / GW;
+    const int so = lane / GW, li = lane % GW;
+    const int c = col0 + li * VEC;          // first column of this lane
+    int32_t sg[VEC];
+#pragma unroll
+    for (int q = 0; q < VEC; q++) sg[q] = oddp[c + q];
+#pragma unroll 4
+    for (int j = 0; j < 32; j += R) {
+        const int slot = j + so;
+        const int32_t b = bases[slot];
+        if (b == -2) continue;
+        const uint32_t word = hs[slot][(li * VEC) >> 2];
+        const int sh = ((li * VEC) & 3) * 8;
+        int32_t key[VEC];
+#pragma unroll
+        for (int q = 0; q < VEC; q++) {
+            const int32_t cnt = (int32_t)((word >> (sh + 8 * q)) & 0xffu);
+            key[q] = sg[q] ? -cnt : cnt;
+        }
+        if (b >= 0) {
+            int32_t base[VEC];
+            const int32_t *bp = sacc + (int64_t)b * dp + c;
+            if constexpr (VEC == 4) {
+                int4 x = __ldcg(reinterpret_cast<const int4 *>(bp));
+                base[0] = x.x; base[1] = x.y; base[2] = x.z; base[3] = x.w;
+            } else {
+#pragma unroll
+                for (int q = 0; q < VEC; q++) base[q] = __ldcg(bp + q);
+            }
+#pragma unroll
+            for (int q = 0; q < VEC; q++) key[q] += base[q];
+        }
+        store_vec<VEC>(out + rowid[slot] * dp + c, key);
+    }
+}
+
+// V2 main pass (one warp = 32 consecutive vertices).
+template <int G>
+__global__ void __launch_bounds__(kThreads) k_v2_walk(DevGame g, int nchunk) {
+    constexpr int NW = 8;
+    __shared__ uint32_t hs[kThreads / 32][32][9];
+    __shared__ int32_t bases[kThreads / 32][32];
+    __shared__ int64_t rowid[kThreads / 32][32];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int64_t N = g.n_int;
+    const uint32_t K = (uint32_t)g.K;
+    if (__ldcg(&g.ctl->spl_overflow)) return;   // host grows the buffers and redoes V2
+    const int32_t *sacc = g.sacc[__ldcg(&g.ctl->spl_final) & 1];
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t tile = blockIdx.x * (int64_t)(blockDim.x >> 5) + wib; tile * 32 < N; tile += nwarps) {
+        const int64_t v = tile * 32 + lane;
+        bool fin = false;
+        uint32_t steps = 0;
+        if (v < N) {
+            unsigned long long e = __ldcg(g.jl + v);
+            fin = (uint32_t)e == (uint32_t)N;
+            uint32_t depth = (uint32_t)(e >> 32);
+            steps = depth < K ? depth : depth % K;
+        }
+        for (int c = 0; c < nchunk; c++) {
+            uint32_t h[NW];
+#pragma unroll
+            for (int q = 0; q < NW; q++) h[q] = 0;
+            int32_t b = -2;
+            if (fin) {
+                int32_t x = walk<NW>(g, (int32_t)v, steps, 32u * c, h);
+                b = (x == (int32_t)N) ? -1 : __ldcg(g.sidx + x);
+            }
+#pragma unroll
+            for (int q = 0; q < NW; q++) hs[wib][lane][q] = h[q];
+            bases[wib][lane] = b;
+            rowid[wib][lane] = v;
+            __syncwarp();
+            write_rows<(G >= 4 ? G / 4 : 1), (G >= 4 ? 4 : G)>(hs[wib], bases[wib], rowid[wib], g.val,
+                                                                g.dp, 32 * c, sacc, g.oddp);
+            __syncwarp();
+        }
+    }
+}
+
+// --------------------------------------------------------------------------
+// Splitter path (only when the deepest finite play has depth >= K).
+// --------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_spl_mark(DevGame g) {
+    if (__ldcg(&g.ctl->maxdepth) < (unsigned long long)g.K) return;
+    const int64_t N = g.n_int;
+    const int lane = threadIdx.x & 31;
+    const int64_t wstride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; base < N; base += wstride) {
+        int64_t v = base + lane;
+        bool is = false;
+        if (v < N) {
+            unsigned long long e = __ldcg(g.jl + v);
+            uint32_t depth = (uint32_t)(e >> 32);
+            is = (uint32_t)e == (uint32_t)N && depth >= (uint32_t)g.K && depth % (uint32_t)g.K == 0;
+        }
+        unsigned mask = __ballot_sync(FULL, is);
+        if (!mask) continue;
+        int leader = __ffs(mask) - 1;
+        unsigned long long b0 = 0;
+        if (lane == leader) b0 = atomicAdd(&g.ctl->nspl, (unsigned long long)__popc(mask));
+        b0 = __shfl_sync(FULL, b0, leader);
+        if (is) {
+            unsigned long long idx = b0 + __popc(mask & ((1u << lane) - 1));
+            if (idx < (unsigned long long)g.spl_cap) {
+                g.sidx[v] = (int32_t)idx;
+                g.spl[idx] = (int32_t)v;
+            } else {
+                g.ctl->spl_overflow = 1;
+            }
+        }
+    }
+}
+
+// seg walk: each splitter walks exactly K steps up to its parent splitter (or sink)
+template <int G>
+__global__ void __launch_bounds__(kThreads) k_spl_seg(DevGame g, int nchunk) {
+    if (__ldcg(&g.ctl->maxdepth) < (unsigned long long)g.K || __ldcg(&g.ctl->spl_overflow)) return;
+    constexpr int NW = 8;
+    __shared__ uint32_t hs[kThreads / 32][32][9];
+    __shared__ int32_t bases[kThreads / 32][32];
+    __shared__ int64_t rowid[kThreads / 32][32];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int64_t S = (int64_t)__ldcg(&g.ctl->nspl);
+    const int64_t N = g.n_int;
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t tile = blockIdx.x * (int64_t)(blockDim.x >> 5) + wib; tile * 32 < S; tile += nwarps) {
+        const int64_t i = tile * 32 + lane;
+        for (int c = 0; c < nchunk; c++) {
+            uint32_t h[NW];
+#pragma unroll
+            for (int q = 0; q < NW; q++) h[q] = 0;
+            int32_t b = -2;
+            if (i < S) {
+                int32_t x = walk<NW>(g, __ldcg(g.spl + i), (uint32_t)g.K, 32u * c, h);
+                if (c == 0) g.sJ[0][i] = (x == (int32_t)N) ? -1 : __ldcg(g.sidx + x);
+                b = -1;
+            }
+#pragma unroll
+            for (int q = 0; q < NW; q++) hs[wib][lane][q] = h[q];
+            bases[wib][lane] = b;
+            rowid[wib][lane] = i;
+            __syncwarp();
+            write_rows<(G >= 4 ? G / 4 : 1), (G >= 4 ? 4 : G)>(hs[wib], bases[wib], rowid[wib],
+                                                                g.sacc[0], g.dp, 32 * c, nullptr, g.oddp);
+            __syncwarp();
+        }
+    }
+}
+
+// Wyllie pointer jumping over the reduced forest: acc[s] += acc[J[s]], J[s] = J[J[s]]
+// (double-buffered, synchronous rounds; cooperative launch).
+__global__ void __launch_bounds__(kThreads) k_spl_wyllie(DevGame g) {
+    if (__ldcg(&g.ctl->maxdepth) < (unsigned long long)g.K || __ldcg(&g.ctl->spl_overflow)) return;
+    const int64_t S = (int64_t)__ldcg(&g.ctl->nspl);
+    const int dp = g.dp;
+    const int64_t total = S * dp;
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int cur = 0, r = 0;
+    for (;;) {
+        const int nx = cur ^ 1;
+        const int32_t *J = g.sJ[cur];
+        const int32_t *A = g.sacc[cur];
+        int32_t *J2 = g.sJ[nx];
+        int32_t *A2 = g.sacc[nx];
+        unsigned long long local = 0;
+        for (int64_t t = tid; t < total; t += stride) {
+            int64_t i = t / dp;
+            int c = (int)(t - i * dp);
+            int32_t j = __ldcg(J + i);
+            int32_t a = __ldcg(A + t);
+            if (j >= 0) {
+                a += __ldcg(A + (int64_t)j * dp + c);
+                if (c == 0) {
+                    int32_t jj = __ldcg(J + j);
+                    J2[i] = jj;
+                    local += (jj >= 0);
+                }
+            } else if (c == 0) {
+                J2[i] = -1;
+            }
+            A2[t] = a;
+        }
+        unsigned long long tot = block_sum(local);
+        if (threadIdx.x == 0 && tot) atomicAdd(&g.ctl->spl_active[r % 3], tot);
+        grid_barrier(g.ctl);
+        unsigned long long act = *(volatile unsigned long long *)&g.ctl->spl_active[r % 3];
+        if (blockIdx.x == 0 && threadIdx.x == 0) g.ctl->spl_active[(r + 2) % 3] = 0;
+        cur = nx;
+        r++;
+        if (act == 0) break;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) g.ctl->spl_final = (unsigned long long)cur;
+}
+
+// --------------------------------------------------------------------------
+// Cycle-dominant priority of ⊤ vertices (pg_valuate / admissibility check):
+// synchronous max-jumping, ceil(log2(N+1)) rounds; cdom(v) = M[J[v]].
+// --------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_cycle_dom(DevGame g, int rounds) {
+    const int64_t N = g.n_int;
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t v = tid; v < N; v += stride) {
+        if (!g.top[v]) continue;
+        g.cJ[0][v] = g.succ[v];
+        g.cmax[0][v] = g.pidx[v];
+    }
+    grid_barrier(g.ctl);
+    int cur = 0;
+    for (int r = 0; r < rounds; r++) {
+        const int nx = cur ^ 1;
+        for (int64_t v = tid; v < N; v += stride) {
+            if (!g.top[v]) continue;
+            int32_t j = __ldcg(g.cJ[cur] + v);
+            int32_t a = __ldcg(g.cmax[cur] + v), b = __ldcg(g.cmax[cur] + j);
+            g.cmax[nx][v] = a > b ? a : b;
+            g.cJ[nx][v] = __ldcg(g.cJ[cur] + j);
+        }
+        grid_barrier(g.ctl);
+        cur = nx;
+    }
+    unsigned long long odd = 0;
+    for (int64_t v = tid; v < N; v += stride) {
+        int32_t cd = -1;
+        if (g.top[v]) {
+            cd = __ldcg(g.cmax[cur] + __ldcg(g.cJ[cur] + v));
+            odd |= g.oddp[cd];
+        }
+        g.cJ[cur ^ 1][v] = cd;   // result array = cJ[cur^1]
+    }
+    if (odd) atomicOr(&g.ctl->odd_cycle, 1ull);
+    if (blockIdx.x == 0 && threadIdx.x == 0) g.ctl->cdom_buf = (unsigned long long)(cur ^ 1);
+}
+
+// --------------------------------------------------------------------------
+// Switch kernels: G lanes per vertex, each lane owning VEC consecutive key
+// columns (16-byte vector loads), lexicographic compare from the highest column
+// via two warp ballots. ODD = All_Odd (argmin over adj, switch iff best ⊏
+// current), !ODD = All_Even (argmax over adj + sink, switch iff current ⊏ best).
+// The current successor is one of the candidates, so its row is taken from the
+// candidate batch instead of being loaded twice.
+// --------------------------------------------------------------------------
+template <int G>
+__device__ __forceinline__ unsigned group_mask(int lane) {
+    if constexpr (G == 32) return FULL;
+    else return ((1u << G) - 1u) << (lane & ~(G - 1));
+}
+
+template <int VEC>
+__device__ __forceinline__ void load_vec(const int32_t *p, int32_t (&r)[VEC]) {
+    if constexpr (VEC == 4) {
+        int4 x = __ldg(reinterpret_cast<const int4 *>(p));
+        r[0] = x.x; r[1] = x.y; r[2] = x.z; r[3] = x.w;
+    } else if constexpr (VEC == 2) {
+        int2 x = __ldg(reinterpret_cast<const int2 *>(p));
+        r[0] = x.x; r[1] = x.y;
+    } else {
+        r[0] = __ldg(p);
+    }
+}
+
+// returns -1 if (ta, ra) ⊏ (tb, rb), +1 if ⊐, 0 if equal (⊤ maximal, ⊤ = ⊤).
+// Must be called warp-uniformly.
+template <int VEC>
+__device__ __forceinline__ int cmp_group(bool ta, const int32_t (&ra)[VEC], bool tb,
+                                         const int32_t (&rb)[VEC], unsigned gm) {
+    bool ne = false, lt = false;
+#pragma unroll
+    for (int q = VEC - 1; q >= 0; q--) {
+        bool dq = ra[q] != rb[q];
+        if (!ne && dq) lt = ra[q] < rb[q];
+        ne = ne || dq;
+    }
+    unsigned nem = __ballot_sync(FULL, ne) & gm;
+    unsigned ltm = __ballot_sync(FULL, lt) & gm;
+    if (ta && tb) return 0;
+    if (ta) return 1;
+    if (tb) return -1;
+    if (!nem) return 0;
+    return ((ltm >> (31u - __clz(nem))) & 1u) ? -1 : 1;
+}
+
+template <int G, int VEC, bool ODD>
+__global__ void __launch_bounds__(kThreads) k_switch(DevGame g) {
+    if (__ldcg(&g.ctl->spl_overflow)) return;
+    constexpr int B = 8;
+    const int lane = threadIdx.x & 31;
+    const int li = lane % G;
+    const unsigned gm = group_mask<G>(lane);
+    const int64_t lo = ODD ? g.n_even : 0;
+    const int64_t hi = ODD ? g.n_int : g.n_even;
+    const int32_t SINK = (int32_t)g.n_int;
+    const int dp = g.dp;
+    constexpr int VPW = 32 / G;   // vertices per warp
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    unsigned long long local = 0, rows = 0;
+    for (int64_t w = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+         lo + w * VPW < hi; w += nwarps) {
+        const int64_t v = lo + w * VPW + lane / G;
+        const bool valid = v < hi;
+        int32_t cur = SINK, ncand = 0;
+        uint32_t beg = 0, end = 0;
+        if (valid) {
+            cur = __ldg(g.succ + v);
+            beg = __ldg(g.rp + v);
+            end = __ldg(g.rp + v + 1);
+            ncand = (int32_t)(end - beg) + (ODD ? 0 : 1);
+        }
+        const int maxc = (int)__reduce_max_sync(FULL, (unsigned)ncand);
+        int32_t best = -1;
+        bool bt = true, ct = false;
+        int32_t br[VEC], cr[VEC];
+#pragma unroll
+        for (int q = 0; q < VEC; q++) { br[q] = 0; cr[q] = 0; }
+        for (int k0 = 0; k0 < maxc; k0 += B) {
+            int32_t c[B];
+            bool t[B];
+            int32_t r[B][VEC];
+#pragma unroll
+            for (int k = 0; k < B; k++) {
+                const int e = k0 + k;
+                c[k] = -1;
+                if (e < ncand) c[k] = (beg + e < end) ? __ldg(g.col + beg + e) : SINK;
+            }
+#pragma unroll
+            for (int k = 0; k < B; k++) t[k] = (c[k] >= 0 && c[k] != SINK) ? (__ldg(g.top + c[k]) != 0) : false;
+#pragma unroll
+            for (int k = 0; k < B; k++) {
+                const bool ld = c[k] >= 0 && c[k] != SINK && !t[k];
+                if (ld) load_vec<VEC>(g.val + (int64_t)c[k] * dp + li * VEC, r[k]);
+                else {
+#pragma unroll
+                    for (int q = 0; q < VEC; q++) r[k][q] = 0;
+                }
+                if (li == 0) rows += ld;
+            }
+#pragma unroll
+            for (int k = 0; k < B; k++) {
+                if (c[k] == cur) {
+                    ct = t[k];
+#pragma unroll
+                    for (int q = 0; q < VEC; q++) cr[q] = r[k][q];
+                }
+                const int cm = cmp_group<VEC>(t[k], r[k], bt, br, gm);
+                const bool take = c[k] >= 0 && (best < 0 || (ODD ? cm < 0 : cm > 0));
+                if (take) {
+                    best = c[k];
+                    bt = t[k];
+#pragma unroll
+                    for (int q = 0; q < VEC; q++) br[q] = r[k][q];
+                }
+            }
+        }
+        const int cm = cmp_group<VEC>(bt, br, ct, cr, gm);
+        const bool sw = valid && best >= 0 && (ODD ? cm < 0 : cm > 0);
+        if (sw && li == 0) g.succ[v] = best;
+        const unsigned bal = __ballot_sync(FULL, sw && li == 0);
+        if (lane == 0) local += __popc(bal);
+    }
+    unsigned long long tot = block_sum(local);
+    if (threadIdx.x == 0 && tot) atomicAdd(ODD ? &g.ctl->odd_switches : &g.ctl->even_switches, tot);
+    rows = block_sum(rows);
+    if (threadIdx.x == 0 && rows) atomicAdd(ODD ? &g.ctl->rows_odd : &g.ctl->rows_even, rows);
+}
+
+// wide rows (dp > 32): one warp per vertex, chunked compare on demand
+__device__ int cmp_wide(const DevGame &g, int32_t a, int32_t b, int lane) {
+    bool ta = g.top[a] != 0, tb = g.top[b] != 0;
+    if (ta && tb) return 0;
+    if (ta) return 1;
+    if (tb) return -1;
+    for (int c = g.dp / 32 - 1; c >= 0; c--) {  // dp > 128: multiple of 32
+        int32_t x = __ldg(g.val + (int64_t)a * g.dp + 32 * c + lane);
+        int32_t y = __ldg(g.val + (int64_t)b * g.dp + 32 * c + lane);
+        unsigned ne = __ballot_sync(FULL, x != y);
+        if (ne) {
+            unsigned lt = __ballot_sync(FULL, x < y);
+            return ((lt >> (31u - __clz(ne))) & 1u) ? -1 : 1;
+        }
+    }
+    return 0;
+}
+
+template <bool ODD>
+__global__ void __launch_bounds__(kThreads) k_switch_wide(DevGame g) {
+    if (__ldcg(&g.ctl->spl_overflow)) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t lo = ODD ? g.n_even : 0;
+    const int64_t hi = ODD ? g.n_int : g.n_even;
+    const int32_t SINK = (int32_t)g.n_int;
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    unsigned long long local = 0;
+    for (int64_t v = lo + blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); v < hi; v += nwarps) {
+        int32_t cur = g.succ[v];
+        uint32_t beg = g.rp[v], end = g.rp[v + 1];
+        int32_t best = g.col[beg];
+        int32_t nc = (int32_t)(end - beg) + (ODD ? 0 : 1);
+        for (int e = 1; e < nc; e++) {
+            int32_t c = (beg + e < end) ? g.col[beg + e] : SINK;
+            int cm = cmp_wide(g, c, best, lane);
+            if (ODD ? cm < 0 : cm > 0) best = c;
+        }
+        int cm = cmp_wide(g, best, cur, lane);
+        bool sw = ODD ? cm < 0 : cm > 0;
+        if (sw && lane == 0) { g.succ[v] = best; local++; }
+    }
+    unsigned long long tot = block_sum(local);
+    if (threadIdx.x == 0 && tot) atomicAdd(ODD ? &g.ctl->odd_switches : &g.ctl->even_switches, tot);
+}
+
+// --------------------------------------------------------------------------
+// exports (device order -> ABI order)
+// --------------------------------------------------------------------------
+__global__ void k_export_val(DevGame g, int64_t count, int32_t *val_out, uint8_t *top_out) {
+    const int d = g.d, dp = g.dp;
+    const int64_t total = count * d;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        int64_t a = t / d;
+        int i = (int)(t - a * d);
+        int32_t v = g.perm[a];
+        bool tp = g.top[v] != 0;
+        if (val_out) {
+            int32_t k = tp ? 0 : g.val[(int64_t)v * dp + i];
+            val_out[t] = g.oddp[i] ? -k : k;
+        }
+        if (top_out && i == 0) top_out[a] = tp ? 1 : 0;
+    }
+}
+
+// which: 0 = Even entries (σ), 1 = Odd entries (τ)
+__global__ void k_export_strategy(DevGame g, int64_t count, int32_t *out, int which, int project) {
+    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < count;
+         a += (int64_t)gridDim.x * blockDim.x) {
+        int32_t v = g.perm[a];
+        int own = v < g.n_even ? 0 : 1;
+        if (own != which) { out[a] = PG_NONE; continue; }
+        int32_t s = g.succ[v];
+        if (s == (int32_t)g.n_int) out[a] = PG_SINK;
+        else out[a] = project ? g.proj[s] : g.iperm[s];
+    }
+}
+
+__global__ void k_export_winner(DevGame g, int64_t count, uint8_t *out) {
+    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < count;
+         a += (int64_t)gridDim.x * blockDim.x)
+        out[a] = g.top[g.perm[a]] ? 0 : 1;
+}
+
+__global__ void k_export_cycle_dom(DevGame g, int64_t count, const int32_t *D, int32_t *out, int which) {
+    const int32_t *res = g.cJ[which];
+    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < count;
+         a += (int64_t)gridDim.x * blockDim.x) {
+        int32_t c = res[g.perm[a]];
+        out[a] = c < 0 ? -1 : D[c];
+    }
+}
+
+// --------------------------------------------------------------------------
+// launchers
+// --------------------------------------------------------------------------
+static LaunchCfg g_lc;
+
+static int grid_for(int64_t items, int per_block = kThreads, int cap_mult = 16) {
+    int64_t b = (items + per_block - 1) / per_block;
+    int64_t cap = (int64_t)g_lc.sms * cap_mult;
+    if (b > cap) b = cap;
+    if (b < 1) b = 1;
+    return (int)b;
+}
+
+cudaError_t setup_launch_cfg(LaunchCfg &lc, int device) {
+    cudaError_t e = cudaDeviceGetAttribute(&lc.sms, cudaDevAttrMultiProcessorCount, device);
+    if (e) return e;
+    int nb = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_v1, kThreads, 0);
+    if (e) return e;
+    lc.coop_v1 = nb * lc.sms;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_spl_wyllie, kThreads, 0);
+    if (e) return e;
+    lc.coop_spl = nb * lc.sms;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_cycle_dom, kThreads, 0);
+    if (e) return e;
+    lc.coop_cyc = nb * lc.sms;
+    g_lc = lc;
+    return cudaSuccess;
+}
+
+static cudaError_t coop(const void *fn, int grid, void **args, cudaStream_t s) {
+    return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, 0, s);
+}
+
+cudaError_t launch_init_profile(const DevGame &g, cudaStream_t s) {
+    k_init_profile<<<grid_for(g.n_int + 1), kThreads, 0, s>>>(g);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_import_strategy(const DevGame &g, const int32_t *abi, int mode, cudaStream_t s) {
+    k_import_strategy<<<grid_for(g.n_int), kThreads, 0, s>>>(g, abi, mode);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_v1(const DevGame &g, const LaunchCfg &lc, cudaStream_t s) {
+    DevGame gg = g;
+    void *args[] = {&gg};
+    int grid = (int)std::min<int64_t>(lc.coop_v1, std::max<int64_t>(1, (g.n_int + kThreads - 1) / kThreads));
+    return coop((const void *)k_v1, grid, args, s);
+}
+
+#define DISPATCH_G(dp, MACRO) \
+    switch (dp) {             \
+        case 1: MACRO(1); break;  \
+        case 2: MACRO(2); break;  \
+        case 4: MACRO(4); break;  \
+        case 8: MACRO(8); break;  \
+        case 16: MACRO(16); break; \
+        default: MACRO(32); break; \
+    }
+
+cudaError_t launch_splitters(const DevGame &g, const LaunchCfg &lc, cudaStream_t s, int *launches) {
+    k_spl_mark<<<grid_for(g.n_int), kThreads, 0, s>>>(g);
+    cudaError_t e = cudaGetLastError();
+    if (e) return e;
+    const int nchunk = g.dp > 32 ? g.dp / 32 : 1;
+    const int grid = grid_for((g.n_int + 31) / 32, kThreads / 32);
+#define SEG(G) k_spl_seg<G><<<grid, kThreads, 0, s>>>(g, nchunk)
+    DISPATCH_G(g.dp, SEG);
+#undef SEG
+    e = cudaGetLastError();
+    if (e) return e;
+    DevGame gg = g;
+    void *args[] = {&gg};
+    e = coop((const void *)k_spl_wyllie, lc.coop_spl, args, s);
+    *launches += 3;
+    return e;
+}
+
+cudaError_t launch_v2(const DevGame &g, cudaStream_t s) {
+    const int nchunk = g.dp > 32 ? g.dp / 32 : 1;
+    const int grid = grid_for((g.n_int + 31) / 32, kThreads / 32);
+#define WALK(G) k_v2_walk<G><<<grid, kThreads, 0, s>>>(g, nchunk)
+    DISPATCH_G(g.dp, WALK);
+#undef WALK
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cycle_dom(const DevGame &g, const LaunchCfg &lc, cudaStream_t s) {
+    int rounds = 1;
+    while ((int64_t(1) << rounds) < g.n_int + 1) rounds++;
+    DevGame gg = g;
+    void *args[] = {&gg, &rounds};
+    return coop((const void *)k_cycle_dom, lc.coop_cyc, args, s);
+}
+
+cudaError_t launch_switch(const DevGame &g, bool odd, cudaStream_t s) {
+    const int64_t nv = odd ? g.n_int - g.n_even : g.n_even;
+    if (nv <= 0) return cudaSuccess;
+    if (g.dp > 128) {
+        const int grid = grid_for(nv, kThreads / 32);
+        if (odd) k_switch_wide<true><<<grid, kThreads, 0, s>>>(g);
+        else k_switch_wide<false><<<grid, kThreads, 0, s>>>(g);
+        return cudaGetLastError();
+    }
+#define SW(G, VEC)                                                               \
+    {                                                                            \
+        const int grid = grid_for((nv + 32 / G - 1) / (32 / G), kThreads / 32);  \
+        if (odd) k_switch<G, VEC, true><<<grid, kThreads, 0, s>>>(g);            \
+        else k_switch<G, VEC, false><<<grid, kThreads, 0, s>>>(g);               \
+    }
+    switch (g.dp) {
+        case 1: SW(1, 1); break;
+        case 2: SW(1, 2); break;
+        case 4: SW(1, 4); break;
+        case 8: SW(2, 4); break;
+        case 16: SW(4, 4); break;
+        case 32: SW(8, 4); break;
+        case 64: SW(16, 4); break;
+        default: SW(32, 4); break;
+    }
+#undef SW
+    return cudaGetLastError();
+}
+
+cudaError_t launch_export_val(const DevGame &g, int64_t count, int32_t *val_out, uint8_t *top_out,
+                              cudaStream_t s) {
+    k_export_val<<<grid_for(count * std::max(g.d, 1)), kThreads, 0, s>>>(g, count, val_out, top_out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_export_strategy(const DevGame &g, int64_t count, int32_t *out, int which,
+                                   bool project, cudaStream_t s) {
+    k_export_strategy<<<grid_for(count), kThreads, 0, s>>>(g, count, out, which, project ? 1 : 0);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_export_winner(const DevGame &g, int64_t count, uint8_t *out, cudaStream_t s) {
+    k_export_winner<<<grid_for(count), kThreads, 0, s>>>(g, count, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_export_cycle_dom(const DevGame &g, int64_t count, const int32_t *D_dev,
+                                    int32_t *out, cudaStream_t s) {
+    // the result buffer index was stored by k_cycle_dom in ctl->cdom_buf; read on host
+    unsigned long long which = 0;
+    cudaError_t e = cudaMemcpyAsync(&which, &g.ctl->cdom_buf, sizeof(which), cudaMemcpyDeviceToHost, s);
+    if (e) return e;
+    e = cudaStreamSynchronize(s);
+    if (e) return e;
+    k_export_cycle_dom<<<grid_for(count), kThreads, 0, s>>>(g, count, D_dev, out, (int)which);
+    return cudaGetLastError();
+}
+
+}  // namespace pgsi
