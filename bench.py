@@ -1,0 +1,333 @@
+#!/usr/bin/env python3
+"""bench.py — valuations/s of greedy all-switches strategy improvement on B200.
+
+Metric (BASELINE.json ``metric``): valuations/s = vertices × inner iterations /
+solve time, on BASELINE.json configs[2] (random parity game, n = 10M, d = 32,
+out-degree 2-5) by default. One *step* = one complete pg_solve (Algorithm 1,
+PAPER.md:548-561: every valuation and every All_Odd / All_Even switch until no
+switch remains) of that game, inputs resident in HBM (pg_load done before the
+timed region). Timing: CUDA events on the library's stream (torch's current
+stream), W untimed warm-up steps, K timed steps bracketed by barrier +
+synchronize, max over ranks. N > 1 GPUs: one independent game per rank
+(weak scaling, no data-path collective).
+
+Extra keys: ``e2e`` = the same metric through the public API from pinned host
+buffers (pg_load incl. host transform + H2D, pg_solve, D2H of winner/σ/τ each
+step); ``roofline`` for the dominant kernel (per-phase CUDA events inside the
+library, PG_PHASE_TIMING); ``cpu_baseline`` = the plain CPU oracle on a bounded
+sample of the same game (rank 0, N = 1); ``clocks`` sampled by NVML during the
+timed region. ``--impl reference`` times the oracle itself (the reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "valuations/sec (vertices×iterations/s) and solve time, 10M-vertex game, 1/2/4/8 B200"
+UNIT = "valuations/s"
+WORKLOADS = {
+    "cfg1": dict(n=1000, d=4, lo=2, hi=3, ref_iters=200, cpu_iters=400,
+                 desc="random parity game n=1,000, d=4, out-degree 2-3 (BASELINE configs[0])"),
+    "cfg2": dict(n=1_000_000, d=16, lo=2, hi=5, ref_iters=4, cpu_iters=40,
+                 desc="random parity game n=1M, d=16, out-degree 2-5 (BASELINE configs[1])"),
+    "cfg3": dict(n=10_000_000, d=32, lo=2, hi=5, ref_iters=1, cpu_iters=3,
+                 desc="random parity game n=10M, d=32, out-degree 2-5 (BASELINE configs[2])"),
+}
+THROTTLE_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+                 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+                 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+
+def measured_peak_gbs():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """NVML sampling of SM clock and clock-event reasons during the timed region."""
+
+    def __init__(self, device_index: int, period_s: float = 0.02):
+        self.period = period_s
+        self.samples = []
+        self.reasons = 0
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            getattr(nv, "nvmlDeviceGetCurrentClocksThrottleReasons")
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.reasons |= int(get_r(self.h))
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["nvml unavailable"]}
+        reasons = [name for bit, name in THROTTLE_BITS.items() if self.reasons & bit]
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def make_game(wl, seed):
+    import pg_inputs as gi
+    return gi.random_game(wl["n"], wl["d"], wl["lo"], wl["hi"], seed)
+
+
+def oracle_sample(game, iters):
+    """Time the plain oracle (as it stands) on the first `iters` valuations of the
+    solve: returns (valuations/s, seconds, iterations done)."""
+    from oracle import Oracle, OracleError
+    o = Oracle(game)                       # load/preprocess: not timed
+    t0 = time.perf_counter()
+    try:
+        r = o.solve(max_inner=iters)
+        done = r.inner_iters
+    except OracleError as e:
+        if e.name != "EITERCAP":
+            raise
+        done = iters
+    dt = time.perf_counter() - t0
+    return game.n * done / dt, dt, done
+
+
+def run_reference(args, wl, rank):
+    """Reference arm: the CPU oracle on the host cores (bounded sample per step)."""
+    if rank != 0:
+        return
+    game = make_game(wl, args.seed)
+    from oracle import build_oracle
+    build_oracle()
+    iters = wl["ref_iters"]
+    for _ in range(args.warmup):
+        oracle_sample(game, iters)
+    tot_units, tot_s = 0.0, 0.0
+    for _ in range(args.steps):
+        v, dt, done = oracle_sample(game, iters)
+        tot_units += game.n * done
+        tot_s += dt
+    value = tot_units / tot_s
+    sample = (f"first {iters} valuation(s) of Algorithm 1 on the {wl['desc']} game per step "
+              f"(oracle load/preprocess excluded)")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot_s / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic", "config": {"workload": wl["desc"], "n": wl["n"], "d": wl["d"],
+                                        "seed": args.seed, "parallelism": "cpu-1thread"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="cfg3", choices=sorted(WORKLOADS))
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e/cpu/clocks)")
+    args = ap.parse_args()
+    wl = WORKLOADS[args.workload]
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, wl, rank)
+        return
+
+    import numpy as np
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1705_02313_b200 import Game, _build
+    _build.build()
+
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    game = make_game(wl, args.seed + rank)   # weak scaling: an independent game per rank
+    G = Game.from_game(game, device=local, stream=stream.cuda_stream, device_ptrs=True,
+                       phase_timing=True)
+    n = game.n
+    out = (torch.empty(n, dtype=torch.uint8, device=dev), torch.empty(n, dtype=torch.int32, device=dev),
+           torch.empty(n, dtype=torch.int32, device=dev), None)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        G.solve(out=out)
+    torch.cuda.synchronize(dev)
+
+    sampler = ClockSampler(local if "CUDA_VISIBLE_DEVICES" not in os.environ else
+                           int(os.environ["CUDA_VISIBLE_DEVICES"].split(",")[local]))
+    acc = {k: 0.0 for k in ("ms_v1", "ms_v2", "ms_odd", "ms_even", "ms_other", "bytes_v1",
+                            "bytes_v2", "bytes_odd", "bytes_even", "n_v1", "n_v2", "n_odd",
+                            "n_even", "gpu_launches", "inner_iters", "outer_passes",
+                            "full_compares", "v1_rounds", "v2_split_valuations")}
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize(dev)
+    with sampler:
+        e0.record(stream)
+        for _ in range(args.steps):
+            r = G.solve(out=out)
+            for k in acc:
+                acc[k] += r.stats[k]
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+    barrier()
+    ms = e0.elapsed_time(e1)
+    units = float(n) * acc["inner_iters"]
+    if dist is not None:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        u = torch.tensor([units], device=dev, dtype=torch.float64)
+        dist.all_reduce(u, op=dist.ReduceOp.SUM)
+        units = float(u.item())
+    value = units / (ms / 1000.0)
+    inner = int(acc["inner_iters"] / args.steps)
+    outer = int(acc["outer_passes"] / args.steps)
+
+    # ---- roofline of the dominant kernel (phase with the largest event time)
+    peak, peak_src = measured_peak_gbs()
+    phases = {p: (acc[f"ms_{p}"], acc[f"bytes_{p}"], acc[f"n_{p}"]) for p in ("v1", "v2", "odd", "even")}
+    kern = {"v1": "k_v1", "v2": "k_spl_*+k_v2_walk", "odd": "k_switch<ODD>", "even": "k_switch<EVEN>"}
+    dom = max(phases, key=lambda p: phases[p][0])
+    dms, dbytes, dn = phases[dom]
+    achieved = dbytes / (dms / 1000.0) / 1e9 if dms > 0 else 0.0
+    total_phase_ms = sum(v[0] for v in phases.values()) + acc["ms_other"]
+    roofline = {"bound": "hbm", "kernel": kern[dom], "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                "bytes_per_launch": dbytes / max(dn, 1), "ms_per_launch": dms / max(dn, 1),
+                "share_of_step": dms / total_phase_ms if total_phase_ms else None,
+                "peak_source": peak_src,
+                "phases": {p: {"ms_per_launch": v[0] / max(v[2], 1),
+                               "GBps": (v[1] / (v[0] / 1000.0) / 1e9) if v[0] else None,
+                               "launches": int(v[2] / args.steps)} for p, v in phases.items()}}
+
+    # ---- end to end through the public API, pinned host buffers
+    e2e = None
+    if not args.no_e2e and not args.profile:
+        def pinned(a):
+            t = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+            return t, t.numpy()
+        keep = [pinned(game.row_ptr), pinned(game.col), pinned(game.owner), pinned(game.priority)]
+        rp, col, own, pri = [k[1] for k in keep]
+        hw = torch.empty(n, dtype=torch.uint8).pin_memory().numpy()
+        hs = torch.empty(n, dtype=torch.int32).pin_memory().numpy()
+        ht = torch.empty(n, dtype=torch.int32).pin_memory().numpy()
+        h2d = rp.nbytes + col.nbytes + own.nbytes + pri.nbytes
+        d2h = hw.nbytes + hs.nbytes + ht.nbytes
+        e2e_steps = max(1, min(args.steps, 3))
+        barrier()
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        e0.record(stream)
+        e_units = 0.0
+        for _ in range(e2e_steps):
+            Ge = Game(n, rp, col, own, pri, device=local, stream=stream.cuda_stream)
+            re = Ge.solve(out=(hw, hs, ht, None))
+            e_units += float(n) * re.stats["inner_iters"]
+            Ge.free()
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        ems = e0.elapsed_time(e1)
+        wall_ms = 1000 * (time.perf_counter() - t0)
+        ems = max(ems, wall_ms)
+        if dist is not None:
+            t = torch.tensor([ems, e_units], device=dev, dtype=torch.float64)
+            tt = t.clone()
+            dist.all_reduce(t[0:1], op=dist.ReduceOp.MAX)
+            dist.all_reduce(tt[1:2], op=dist.ReduceOp.SUM)
+            ems, e_units = float(t[0].item()), float(tt[1].item())
+        e2e = {"value": e_units / (ems / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "ms_per_step": ems / e2e_steps, "steps": e2e_steps,
+               "includes": "pg_load (validate, canonicalise, preprocess on host; H2D) + pg_solve + D2H"}
+
+    # ---- CPU oracle baseline (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
+        from oracle import build_oracle
+        build_oracle()
+        v, dt, done = oracle_sample(game, wl["cpu_iters"])
+        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"first {done} valuations of Algorithm 1 on this game ({dt:.1f} s, "
+                         f"1 host thread, oracle load excluded)"}
+
+    if rank == 0:
+        val_bytes = (G.n_internal + 1) * 4 * max(1, 1 << (max(G.d, 1) - 1).bit_length())
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": {"workload": wl["desc"], "n": n, "d": G.d, "out_degree": f"{wl['lo']}-{wl['hi']}",
+                       "seed": args.seed, "n_internal": G.n_internal, "m": int(game.m),
+                       "inner_iters": inner, "outer_passes": outer, "solve_ms": ms / args.steps,
+                       "full_compares_per_solve": int(acc["full_compares"] / args.steps),
+                       "v1_rounds_per_solve": int(acc["v1_rounds"] / args.steps),
+                       "split_valuations_per_solve": int(acc["v2_split_valuations"] / args.steps),
+                       "parallelism": "single GPU" if world == 1 else f"weak: {world} independent games",
+                       "l2": f"inputs larger than L2: valuation table {val_bytes / 1e9:.2f} GB > 126 MB"},
+            "roofline": roofline,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": sampler.summary(),
+            "gpu_launches": int(acc["gpu_launches"]),
+        }
+        print(json.dumps(line), flush=True)
+    G.free()
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

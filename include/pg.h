@@ -88,7 +88,8 @@ typedef struct {
     int32_t device;       /* CUDA device ordinal                                       */
     void *stream;         /* cudaStream_t to run on; NULL = the handle creates its own */
     int32_t splitter_k;   /* V2 splitter depth stride (0 = default 32; 1..255)          */
-    int32_t reserved;
+    int32_t prefix_pairs; /* (column,key) pairs per compact prefix (0 = default 7; 1..7);
+                             fewer pairs only force more full-row compares (testing)   */
     int64_t max_inner;    /* cap on total inner iterations per call (0 = none)         */
     int64_t max_outer;    /* cap on outer passes per pg_solve (0 = none)               */
 } pg_options;
@@ -107,12 +108,14 @@ typedef struct {
     double ms_v1, ms_v2, ms_odd, ms_even, ms_other; /* PG_PHASE_TIMING: CUDA-event totals */
     int64_t n_v1, n_v2, n_odd, n_even;   /* PG_PHASE_TIMING: launches per phase            */
     /* algorithmic HBM bytes summed over the call:
-     * V1   = 5·n'             (succ read, ⊤ flag write)
-     * V2   = n' + R·n_fin     (priority index read, one row write per finite vertex)
-     * odd  = 4(n_odd+1) + 4·n_odd + (4+1)·m_odd + n_odd + R·rows_odd + 4·switched
-     * even = 4(n_even+1) + 4·n_even + (4+1)·m_even + n_even + R·rows_even + 4·switched
-     * with R = 4·dp row bytes and rows_* = finite non-sink rows the kernel gathered. */
+     * V1   = 5·n'                    (succ read, ⊤ flag write)
+     * V2   = n' + R·n_fin + 32·n'    (priority index read, one key row per finite vertex,
+     *                                 one 32-byte compact prefix per vertex)
+     * odd  = 4(n_odd+1) + 4·n_odd + 4·m_odd + 32·prefixes + 2R·full_compares + 4·switched
+     * even = 4(n_even+1) + 4·n_even + 4·m_even + 32·prefixes + 2R·full_compares + 4·switched
+     * with R = 4·dp row bytes, prefixes = non-sink candidate prefixes gathered. */
     double bytes_v1, bytes_v2, bytes_odd, bytes_even;
+    int64_t full_compares;   /* switch comparisons the compact prefixes could not decide */
 } pg_stats;
 
 /* pg_load: validate, canonicalise and preprocess a game, copy it to the GPU.

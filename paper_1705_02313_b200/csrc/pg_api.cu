@@ -169,7 +169,7 @@ pg_status grow_splitters(pg_game h, int64_t need) {
 }
 
 // One valuation of the current profile (σ ∪ τ in G.succ): V1 then V2.
-pg_status valuate_dev(pg_game h, bool want_cdom) {
+pg_status valuate_dev(pg_game h, bool want_cdom, bool full_rows) {
     if (want_cdom && !h->G.cJ[0]) {    // cycle-dominant scratch, allocated on first use
         const size_t N1 = (size_t)h->G.n_int + 1;
         CK(h, dalloc(h, &h->G.cJ[0], N1));
@@ -187,7 +187,7 @@ pg_status valuate_dev(pg_game h, bool want_cdom) {
         PhaseScope ps(h, PH_V2);
         int launches = 0;
         CK(h, launch_splitters(h->G, h->lc, h->stream, &launches));
-        CK(h, launch_v2(h->G, h->stream));
+        CK(h, launch_v2(h->G, h->stream, full_rows));
         h->st.gpu_launches += launches + 1;
     }
     if (want_cdom) {
@@ -204,10 +204,10 @@ pg_status readback(pg_game h) {
     return PG_OK;
 }
 
-void note_valuation(pg_game h) {
+void note_valuation(pg_game h, bool full_rows) {
     const double np_ = (double)h->G.n_int, R = 4.0 * h->G.dp;
     h->st.bytes_v1 += 5.0 * np_;
-    h->st.bytes_v2 += np_ + R * (double)h->h_ctl->n_fin;
+    h->st.bytes_v2 += np_ + (full_rows ? R * (double)h->h_ctl->n_fin : 32.0 * np_);
     h->st.v1_rounds += (int64_t)h->h_ctl->v1_rounds;
     if ((int64_t)h->h_ctl->maxdepth > h->st.max_depth) h->st.max_depth = (int64_t)h->h_ctl->maxdepth;
     if ((int64_t)h->h_ctl->maxdepth >= h->G.K) h->st.v2_split_valuations++;
@@ -216,12 +216,12 @@ void note_valuation(pg_game h) {
 // valuation + one switch step, redone if the splitter buffers overflowed.
 pg_status valuate_and_switch(pg_game h, bool odd, bool want_cdom, bool do_switch) {
     for (;;) {
-        pg_status rc = valuate_dev(h, want_cdom);
+        pg_status rc = valuate_dev(h, want_cdom, !do_switch);
         if (rc) return rc;
         if (do_switch) {
             PhaseScope ps(h, odd ? PH_ODD : PH_EVEN);
             CK(h, launch_switch(h->G, odd, h->stream));
-            h->st.gpu_launches += 1;
+            h->st.gpu_launches += 3;
         }
         rc = readback(h);
         if (rc) return rc;
@@ -229,7 +229,7 @@ pg_status valuate_and_switch(pg_game h, bool odd, bool want_cdom, bool do_switch
         rc = grow_splitters(h, (int64_t)h->h_ctl->nspl);   // rare: redo with larger buffers
         if (rc) return rc;
     }
-    note_valuation(h);
+    note_valuation(h, !do_switch);
     return PG_OK;
 }
 
@@ -251,8 +251,9 @@ pg_status inner_loop(pg_game h, int64_t *inner, bool check) {
         h->st.odd_switches += c;
         {
             const double no = (double)(h->G.n_int - h->G.n_even), mo = (double)h->m_odd;
-            h->st.bytes_odd += 4.0 * (no + 1) + 4.0 * no + 5.0 * mo + no +
-                               4.0 * h->G.dp * (double)h->h_ctl->rows_odd + 4.0 * c;
+            h->st.bytes_odd += 4.0 * (no + 1) + 4.0 * no + 4.0 * mo + 32.0 * (double)h->h_ctl->rows_odd +
+                               8.0 * h->G.dp * (double)h->h_ctl->full_odd + 4.0 * c;
+            h->st.full_compares += (int64_t)h->h_ctl->full_odd;
         }
         if (c == 0) return PG_OK;
     }
@@ -261,10 +262,11 @@ pg_status inner_loop(pg_game h, int64_t *inner, bool check) {
 pg_status even_switch(pg_game h, int64_t *count) {
     CK(h, cudaMemsetAsync(&h->G.ctl->even_switches, 0, sizeof(unsigned long long), h->stream));
     CK(h, cudaMemsetAsync(&h->G.ctl->rows_even, 0, sizeof(unsigned long long), h->stream));
+    CK(h, cudaMemsetAsync(&h->G.ctl->full_even, 0, sizeof(unsigned long long), h->stream));
     {
         PhaseScope ps(h, PH_EVEN);
         CK(h, launch_switch(h->G, false, h->stream));
-        h->st.gpu_launches += 1;
+        h->st.gpu_launches += 3;
     }
     pg_status rc = readback(h);
     if (rc) return rc;
@@ -272,8 +274,9 @@ pg_status even_switch(pg_game h, int64_t *count) {
     h->st.even_switches += *count;
     {
         const double ne = (double)h->G.n_even, me = (double)(h->m_int - h->m_odd);
-        h->st.bytes_even += 4.0 * (ne + 1) + 4.0 * ne + 5.0 * me + ne +
-                            4.0 * h->G.dp * (double)h->h_ctl->rows_even + 4.0 * *count;
+        h->st.bytes_even += 4.0 * (ne + 1) + 4.0 * ne + 4.0 * me + 32.0 * (double)h->h_ctl->rows_even +
+                            8.0 * h->G.dp * (double)h->h_ctl->full_even + 4.0 * *count;
+        h->st.full_compares += (int64_t)h->h_ctl->full_even;
     }
     return PG_OK;
 }
@@ -417,6 +420,7 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     else dp = (H.d + 31) / 32 * 32;
     G.dp = dp;
     G.K = o.splitter_k > 0 ? std::min(o.splitter_k, 255) : 32;
+    G.cpx_pairs = (o.prefix_pairs >= 1 && o.prefix_pairs <= 7) ? o.prefix_pairs : 7;
     const size_t N1 = (size_t)H.n_int + 1;
     uint32_t *rp; int32_t *colp; uint8_t *pidx, *oddp;
     int32_t *perm, *iperm, *proj;
@@ -428,6 +432,9 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     CKL(dalloc(h, &G.jl, N1));
     CKL(dalloc(h, &G.top, N1));
     CKL(dalloc(h, &G.val, N1 * dp));
+    CKL(dalloc(h, &G.cpx, N1 * 8));
+    CKL(dalloc(h, &G.hard, N1));
+    CKL(dalloc(h, &G.swl, N1));
     CKL(dalloc(h, &G.sidx, N1));
     CKL(dalloc(h, &perm, (size_t)H.n_int));
     CKL(dalloc(h, &iperm, (size_t)H.n_int));
@@ -452,6 +459,7 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     if (H.d) CKL(cudaMemcpyAsync(h->d_D, H.D.data(), sizeof(int32_t) * H.d, cudaMemcpyHostToDevice, s));
     CKL(cudaMemsetAsync(G.val, 0, sizeof(int32_t) * N1 * dp, s));   // sink row = 0
     CKL(cudaMemsetAsync(G.top, 0, N1, s));
+    CKL(cudaMemsetAsync(G.cpx, 0, sizeof(uint32_t) * N1 * 8, s));   // sink prefix = zero row
     CKL(cudaMemsetAsync(G.ctl, 0, sizeof(Ctl), s));
     // splitter buffers: grown on demand (overflow protocol in valuate_and_switch)
     {
@@ -569,6 +577,7 @@ pg_status pg_best_response(pg_game h, const int32_t *sigma, const int32_t *tau0,
                                 {top, nullptr, (size_t)N}};
     if ((rc = outputs_begin(h, outs))) return rc;
     if (N && tau_out) CK(h, launch_export_strategy(h->G, N, (int32_t *)outs[0].dev, 1, false, h->stream));
+    if (N && val) { CK(h, launch_v2(h->G, h->stream, true)); h->st.gpu_launches++; }   // full rows for output
     if (N && (val || top)) CK(h, launch_export_val(h->G, N, (int32_t *)outs[1].dev, (uint8_t *)outs[2].dev, h->stream));
     if ((rc = outputs_end(h, outs))) return rc;
     timing_collect(h);
@@ -622,7 +631,11 @@ pg_status pg_solve(pg_game h, uint8_t *winner, int32_t *sigma, int32_t *tau, int
         h->st.gpu_launches += 1;
         if (sigma) { CK(h, launch_export_strategy(h->G, n, (int32_t *)outs[1].dev, 0, false, h->stream)); h->st.gpu_launches++; }
         if (tau) { CK(h, launch_export_strategy(h->G, n, (int32_t *)outs[2].dev, 1, true, h->stream)); h->st.gpu_launches++; }
-        if (val) { CK(h, launch_export_val(h->G, n, (int32_t *)outs[3].dev, nullptr, h->stream)); h->st.gpu_launches++; }
+        if (val) {
+            CK(h, launch_v2(h->G, h->stream, true));   // full rows of val^{σ*} for output
+            CK(h, launch_export_val(h->G, n, (int32_t *)outs[3].dev, nullptr, h->stream));
+            h->st.gpu_launches += 2;
+        }
     }
     if ((rc = outputs_end(h, outs))) return rc;
     timing_collect(h);

@@ -44,8 +44,12 @@ struct Ctl {
     unsigned long long even_switches;
     unsigned long long cdom_buf;    // which cJ buffer holds cycle_dom (pidx or -1)
     unsigned long long n_fin;       // finite vertices of the last valuation
-    unsigned long long rows_odd;    // rows gathered by the last All_Odd launch
-    unsigned long long rows_even;   // rows gathered by the last All_Even launch
+    unsigned long long rows_odd;    // compact prefixes gathered by the last All_Odd launch
+    unsigned long long rows_even;   // compact prefixes gathered by the last All_Even launch
+    unsigned long long full_odd;    // full-row compares (undecided prefixes), All_Odd
+    unsigned long long full_even;   // full-row compares, All_Even
+    unsigned long long nhard;       // vertices deferred to the hard (full-compare) pass
+    unsigned long long nswl;        // switches recorded by the current switch step (must follow nhard)
     // ---- not reset per valuation ----
     unsigned long long bad_index;   // ULLONG_MAX = none, else min invalid ABI index
     unsigned int bar_count;         // grid barrier
@@ -60,6 +64,7 @@ struct DevGame {
     int32_t dp;         // padded row width (pow2 <= 128, else multiple of 32)
     int32_t K;          // splitter depth stride
     int64_t spl_cap;    // capacity of spl / sJ / sacc (rows)
+    int32_t cpx_pairs;  // (column, key) pairs kept in a compact prefix (1..7; tests shrink it)
     const uint32_t *rp;
     const int32_t *col;
     const uint8_t *pidx;
@@ -68,6 +73,9 @@ struct DevGame {
     unsigned long long *jl;
     uint8_t *top;
     int32_t *val;
+    uint32_t *cpx;      // compact prefixes, 8 words per vertex (+ sink row of zeros)
+    int32_t *hard;      // switch worklist of vertices with undecided prefixes
+    int2 *swl;          // (vertex, new successor) switches of the current step
     int32_t *sidx;
     int32_t *spl;
     int32_t *sJ[2];
@@ -93,7 +101,7 @@ cudaError_t launch_import_strategy(const DevGame &g, const int32_t *abi_strategy
                                    cudaStream_t s);
 cudaError_t launch_v1(const DevGame &g, const LaunchCfg &lc, cudaStream_t s);
 cudaError_t launch_splitters(const DevGame &g, const LaunchCfg &lc, cudaStream_t s, int *launches);
-cudaError_t launch_v2(const DevGame &g, cudaStream_t s);
+cudaError_t launch_v2(const DevGame &g, cudaStream_t s, bool full_rows);
 cudaError_t launch_cycle_dom(const DevGame &g, const LaunchCfg &lc, cudaStream_t s);
 cudaError_t launch_switch(const DevGame &g, bool odd, cudaStream_t s);
 cudaError_t launch_export_val(const DevGame &g, int64_t count, int32_t *val_out, uint8_t *top_out,

@@ -254,9 +254,86 @@ __device__ __forceinline__ void write_rows(uint32_t (*hs)[9], const int32_t *bas
     }
 }
 
-// V2 main pass (one warp = 32 consecutive vertices).
+// --------------------------------------------------------------------------
+// Compact prefix of a valuation row: 8 words =
+// header (bit0 = ⊤, bit1 = truncated) + the 7 highest nonzero key columns as
+// order-preserving int32 pairs e(col, key) = ±((col << 23) + min(|key|, CAP)).
+// Comparing two prefixes word by word (signed) decides ⊑ exactly (PAPER.md:
+// 374-383: maxdiff is the first differing (column, key) pair from the top) unless
+// both agree on every stored pair and one is truncated — then the full rows
+// decide (rare; counted in stats).
+// --------------------------------------------------------------------------
+constexpr uint32_t kCap = (1u << 23) - 2;
+
+struct Cpx {
+    uint32_t w[8];
+    int np;
+    bool trunc;
+};
+
+__device__ __forceinline__ void cpx_init(Cpx &p) {
+#pragma unroll
+    for (int k = 0; k < 8; k++) p.w[k] = 0;
+    p.np = 0;
+    p.trunc = false;
+}
+
+__device__ __forceinline__ void cpx_emit(Cpx &p, int col, int32_t key, int maxp) {
+    if (key == 0 || p.trunc) return;
+    if (p.np >= maxp) { p.trunc = true; return; }
+    uint32_t mag = (uint32_t)(key < 0 ? -key : key);
+    const bool cap = mag >= kCap;
+    if (cap) mag = kCap;
+    int32_t e = (int32_t)(((uint32_t)col << 23) + mag);
+    e = key > 0 ? e : -e;
+#pragma unroll
+    for (int k = 0; k < 7; k++)
+        if (p.np == k) p.w[k + 1] = (uint32_t)e;
+    p.np++;
+    if (cap) p.trunc = true;
+}
+
+// emit the nonzero keys of one 32-column chunk (columns 32c+31 .. 32c), top-down.
+// Without a base row only the nonzero histogram bytes are visited.
+__device__ __forceinline__ void cpx_chunk(Cpx &p, const uint32_t (&h)[8], const int32_t *brow,
+                                          int col0, int dp, const uint8_t *oddp, int maxp) {
+    if (!brow) {
+#pragma unroll
+        for (int w = 7; w >= 0; w--) {
+            uint32_t word = h[w];
+            while (word && !p.trunc) {
+                const int q = (31 - __clz(word)) >> 3;
+                const int col = col0 + 4 * w + q;
+                const int32_t cnt = (int32_t)((word >> (8 * q)) & 0xffu);
+                word &= ~(0xffu << (8 * q));
+                cpx_emit(p, col, oddp[col] ? -cnt : cnt, maxp);
+            }
+        }
+        return;
+    }
+    for (int col = min(col0 + 31, dp - 1); col >= col0 && !p.trunc; col--) {
+        const int w = (col - col0) >> 2, q = (col - col0) & 3;
+        uint32_t word = 0;
+#pragma unroll
+        for (int k = 0; k < 8; k++) if (k == w) word = h[k];
+        const int32_t cnt = (int32_t)((word >> (8 * q)) & 0xffu);
+        const int32_t bk = __ldcg(brow + col);
+        if (cnt == 0 && bk == 0) continue;
+        cpx_emit(p, col, oddp[col] ? bk - cnt : bk + cnt, maxp);
+    }
+}
+
+__device__ __forceinline__ void cpx_store(uint32_t *cpx, int64_t v, const Cpx &p, bool top) {
+    uint4 *dst = reinterpret_cast<uint4 *>(cpx + v * 8);
+    const uint32_t hdr = top ? 1u : (p.trunc ? 2u : 0u);
+    dst[0] = make_uint4(hdr, p.w[1], p.w[2], p.w[3]);
+    dst[1] = make_uint4(p.w[4], p.w[5], p.w[6], p.w[7]);
+}
+
+// V2, full-row form (outputs only: pg_valuate, val of pg_solve / pg_best_response):
+// one warp = 32 consecutive vertices, rows written cooperatively.
 template <int G>
-__global__ void __launch_bounds__(kThreads) k_v2_walk(DevGame g, int nchunk) {
+__global__ void __launch_bounds__(kThreads) k_v2_rows(DevGame g, int nchunk) {
     constexpr int NW = 8;
     __shared__ uint32_t hs[kThreads / 32][32][9];
     __shared__ int32_t bases[kThreads / 32][32];
@@ -295,6 +372,37 @@ __global__ void __launch_bounds__(kThreads) k_v2_walk(DevGame g, int nchunk) {
                                                                 g.dp, 32 * c, sacc, g.oddp);
             __syncwarp();
         }
+    }
+}
+
+// V2, compact form (the solve loop): one thread per vertex walks its play to the
+// sink or the nearest splitter (≤ K-1 steps), adds the
+// splitter's row when there is one, and stores the 32-byte compact prefix; ⊤
+// vertices store the ⊤ header. Full key rows are not materialised.
+__global__ void __launch_bounds__(kThreads) k_v2_cpx(DevGame g, int nchunk) {
+    if (__ldcg(&g.ctl->spl_overflow)) return;   // host grows the buffers and redoes V2
+    const int64_t N = g.n_int;
+    const uint32_t K = (uint32_t)g.K;
+    const int32_t *sacc = g.sacc[__ldcg(&g.ctl->spl_final) & 1];
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < N;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long e = __ldcg(g.jl + v);
+        const bool fin = (uint32_t)e == (uint32_t)N;
+        Cpx p;
+        cpx_init(p);
+        if (fin) {
+            const uint32_t depth = (uint32_t)(e >> 32);
+            const uint32_t steps = depth < K ? depth : depth % K;
+            for (int c = nchunk - 1; c >= 0 && !p.trunc; c--) {
+                uint32_t h[8];
+#pragma unroll
+                for (int q = 0; q < 8; q++) h[q] = 0;
+                const int32_t x = walk<8>(g, (int32_t)v, steps, 32u * c, h);
+                const int32_t b = (x == (int32_t)N) ? -1 : __ldcg(g.sidx + x);
+                cpx_chunk(p, h, b >= 0 ? sacc + (int64_t)b * g.dp : nullptr, 32 * c, g.dp, g.oddp, g.cpx_pairs);
+            }
+        }
+        cpx_store(g.cpx, v, p, !fin);
     }
 }
 
@@ -455,179 +563,169 @@ __global__ void __launch_bounds__(kThreads) k_cycle_dom(DevGame g, int rounds) {
 }
 
 // --------------------------------------------------------------------------
-// Switch kernels: G lanes per vertex, each lane owning VEC consecutive key
-// columns (16-byte vector loads), lexicographic compare from the highest column
-// via two warp ballots. ODD = All_Odd (argmin over adj, switch iff best ⊏
-// current), !ODD = All_Even (argmax over adj + sink, switch iff current ⊏ best).
-// The current successor is one of the candidates, so its row is taken from the
-// candidate batch instead of being loaded twice.
+// Switch kernels (All_Odd; All_Even, PAPER.md:416-434,
+// 487-491): one thread per vertex. Candidates are scanned in canonical order
+// (adjacency, then the sink for Even: reading 3) comparing 32-byte compact
+// prefixes; an undecided comparison falls back to the full key rows. Strict
+// switches only (reading 5). The current successor is a candidate, so its
+// prefix comes from the candidate batch.
 // --------------------------------------------------------------------------
-template <int G>
-__device__ __forceinline__ unsigned group_mask(int lane) {
-    if constexpr (G == 32) return FULL;
-    else return ((1u << G) - 1u) << (lane & ~(G - 1));
+// -1 / 0 / +1, or 2 when the prefixes cannot decide.
+__device__ __forceinline__ int cmp_cpx(const uint32_t (&a)[8], const uint32_t (&b)[8]) {
+    const bool ta = a[0] & 1u, tb = b[0] & 1u;
+    if (ta || tb) return ta == tb ? 0 : (ta ? 1 : -1);
+#pragma unroll
+    for (int j = 1; j < 8; j++)
+        if (a[j] != b[j]) return (int32_t)a[j] < (int32_t)b[j] ? -1 : 1;
+    return ((a[0] | b[0]) & 2u) ? 2 : 0;
 }
 
-template <int VEC>
-__device__ __forceinline__ void load_vec(const int32_t *p, int32_t (&r)[VEC]) {
-    if constexpr (VEC == 4) {
-        int4 x = __ldg(reinterpret_cast<const int4 *>(p));
-        r[0] = x.x; r[1] = x.y; r[2] = x.z; r[3] = x.w;
-    } else if constexpr (VEC == 2) {
-        int2 x = __ldg(reinterpret_cast<const int2 *>(p));
-        r[0] = x.x; r[1] = x.y;
-    } else {
-        r[0] = __ldg(p);
-    }
+// Full lexicographic compare of val(a), val(b) (finite, or the sink) when the
+// prefixes tie: both rows are rebuilt chunk by chunk, highest chunk first, by
+// re-walking the plays (as V2 does) — full rows are not kept in HBM.
+__device__ __forceinline__ int32_t walk_row(const DevGame &g, int32_t x, int c, uint32_t (&h)[8],
+                                            const int32_t *sacc) {
+#pragma unroll
+    for (int q = 0; q < 8; q++) h[q] = 0;
+    const int32_t N = (int32_t)g.n_int;
+    if (x == N) return -1;
+    const unsigned long long e = __ldcg(g.jl + x);
+    const uint32_t depth = (uint32_t)(e >> 32), K = (uint32_t)g.K;
+    const int32_t y = walk<8>(g, x, depth < K ? depth : depth % K, 32u * c, h);
+    return (y == N) ? -1 : __ldcg(g.sidx + y);
 }
 
-// returns -1 if (ta, ra) ⊏ (tb, rb), +1 if ⊐, 0 if equal (⊤ maximal, ⊤ = ⊤).
-// Must be called warp-uniformly.
-template <int VEC>
-__device__ __forceinline__ int cmp_group(bool ta, const int32_t (&ra)[VEC], bool tb,
-                                         const int32_t (&rb)[VEC], unsigned gm) {
-    bool ne = false, lt = false;
+__device__ __noinline__ int cmp_full(const DevGame &g, int32_t a, int32_t b) {
+    const int32_t *sacc = g.sacc[__ldcg(&g.ctl->spl_final) & 1];
+    const int nchunk = g.dp > 32 ? g.dp / 32 : 1;
+    for (int c = nchunk - 1; c >= 0; c--) {
+        uint32_t ha[8], hb[8];
+        const int32_t ba = walk_row(g, a, c, ha, sacc);
+        const int32_t bb = walk_row(g, b, c, hb, sacc);
+        for (int col = min(32 * c + 31, g.dp - 1); col >= 32 * c; col--) {
+            const int w = (col - 32 * c) >> 2, q = (col - 32 * c) & 3;
+            uint32_t wa = 0, wb = 0;
 #pragma unroll
-    for (int q = VEC - 1; q >= 0; q--) {
-        bool dq = ra[q] != rb[q];
-        if (!ne && dq) lt = ra[q] < rb[q];
-        ne = ne || dq;
-    }
-    unsigned nem = __ballot_sync(FULL, ne) & gm;
-    unsigned ltm = __ballot_sync(FULL, lt) & gm;
-    if (ta && tb) return 0;
-    if (ta) return 1;
-    if (tb) return -1;
-    if (!nem) return 0;
-    return ((ltm >> (31u - __clz(nem))) & 1u) ? -1 : 1;
-}
-
-template <int G, int VEC, bool ODD>
-__global__ void __launch_bounds__(kThreads) k_switch(DevGame g) {
-    if (__ldcg(&g.ctl->spl_overflow)) return;
-    constexpr int B = 8;
-    const int lane = threadIdx.x & 31;
-    const int li = lane % G;
-    const unsigned gm = group_mask<G>(lane);
-    const int64_t lo = ODD ? g.n_even : 0;
-    const int64_t hi = ODD ? g.n_int : g.n_even;
-    const int32_t SINK = (int32_t)g.n_int;
-    const int dp = g.dp;
-    constexpr int VPW = 32 / G;   // vertices per warp
-    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    unsigned long long local = 0, rows = 0;
-    for (int64_t w = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
-         lo + w * VPW < hi; w += nwarps) {
-        const int64_t v = lo + w * VPW + lane / G;
-        const bool valid = v < hi;
-        int32_t cur = SINK, ncand = 0;
-        uint32_t beg = 0, end = 0;
-        if (valid) {
-            cur = __ldg(g.succ + v);
-            beg = __ldg(g.rp + v);
-            end = __ldg(g.rp + v + 1);
-            ncand = (int32_t)(end - beg) + (ODD ? 0 : 1);
-        }
-        const int maxc = (int)__reduce_max_sync(FULL, (unsigned)ncand);
-        int32_t best = -1;
-        bool bt = true, ct = false;
-        int32_t br[VEC], cr[VEC];
-#pragma unroll
-        for (int q = 0; q < VEC; q++) { br[q] = 0; cr[q] = 0; }
-        for (int k0 = 0; k0 < maxc; k0 += B) {
-            int32_t c[B];
-            bool t[B];
-            int32_t r[B][VEC];
-#pragma unroll
-            for (int k = 0; k < B; k++) {
-                const int e = k0 + k;
-                c[k] = -1;
-                if (e < ncand) c[k] = (beg + e < end) ? __ldg(g.col + beg + e) : SINK;
-            }
-#pragma unroll
-            for (int k = 0; k < B; k++) t[k] = (c[k] >= 0 && c[k] != SINK) ? (__ldg(g.top + c[k]) != 0) : false;
-#pragma unroll
-            for (int k = 0; k < B; k++) {
-                const bool ld = c[k] >= 0 && c[k] != SINK && !t[k];
-                if (ld) load_vec<VEC>(g.val + (int64_t)c[k] * dp + li * VEC, r[k]);
-                else {
-#pragma unroll
-                    for (int q = 0; q < VEC; q++) r[k][q] = 0;
-                }
-                if (li == 0) rows += ld;
-            }
-#pragma unroll
-            for (int k = 0; k < B; k++) {
-                if (c[k] == cur) {
-                    ct = t[k];
-#pragma unroll
-                    for (int q = 0; q < VEC; q++) cr[q] = r[k][q];
-                }
-                const int cm = cmp_group<VEC>(t[k], r[k], bt, br, gm);
-                const bool take = c[k] >= 0 && (best < 0 || (ODD ? cm < 0 : cm > 0));
-                if (take) {
-                    best = c[k];
-                    bt = t[k];
-#pragma unroll
-                    for (int q = 0; q < VEC; q++) br[q] = r[k][q];
-                }
-            }
-        }
-        const int cm = cmp_group<VEC>(bt, br, ct, cr, gm);
-        const bool sw = valid && best >= 0 && (ODD ? cm < 0 : cm > 0);
-        if (sw && li == 0) g.succ[v] = best;
-        const unsigned bal = __ballot_sync(FULL, sw && li == 0);
-        if (lane == 0) local += __popc(bal);
-    }
-    unsigned long long tot = block_sum(local);
-    if (threadIdx.x == 0 && tot) atomicAdd(ODD ? &g.ctl->odd_switches : &g.ctl->even_switches, tot);
-    rows = block_sum(rows);
-    if (threadIdx.x == 0 && rows) atomicAdd(ODD ? &g.ctl->rows_odd : &g.ctl->rows_even, rows);
-}
-
-// wide rows (dp > 32): one warp per vertex, chunked compare on demand
-__device__ int cmp_wide(const DevGame &g, int32_t a, int32_t b, int lane) {
-    bool ta = g.top[a] != 0, tb = g.top[b] != 0;
-    if (ta && tb) return 0;
-    if (ta) return 1;
-    if (tb) return -1;
-    for (int c = g.dp / 32 - 1; c >= 0; c--) {  // dp > 128: multiple of 32
-        int32_t x = __ldg(g.val + (int64_t)a * g.dp + 32 * c + lane);
-        int32_t y = __ldg(g.val + (int64_t)b * g.dp + 32 * c + lane);
-        unsigned ne = __ballot_sync(FULL, x != y);
-        if (ne) {
-            unsigned lt = __ballot_sync(FULL, x < y);
-            return ((lt >> (31u - __clz(ne))) & 1u) ? -1 : 1;
+            for (int k = 0; k < 8; k++) if (k == w) { wa = ha[k]; wb = hb[k]; }
+            int32_t ka = (int32_t)((wa >> (8 * q)) & 0xffu), kb = (int32_t)((wb >> (8 * q)) & 0xffu);
+            if (g.oddp[col]) { ka = -ka; kb = -kb; }
+            if (ba >= 0) ka += __ldcg(sacc + (int64_t)ba * g.dp + col);
+            if (bb >= 0) kb += __ldcg(sacc + (int64_t)bb * g.dp + col);
+            if (ka != kb) return ka < kb ? -1 : 1;
         }
     }
     return 0;
 }
 
-template <bool ODD>
-__global__ void __launch_bounds__(kThreads) k_switch_wide(DevGame g) {
-    if (__ldcg(&g.ctl->spl_overflow)) return;
-    const int lane = threadIdx.x & 31;
-    const int64_t lo = ODD ? g.n_even : 0;
-    const int64_t hi = ODD ? g.n_int : g.n_even;
+// One vertex of All_Odd / All_Even. HARD = false: compact prefixes only; a vertex
+// meeting an undecided comparison is appended to the hard list and left
+// unchanged. HARD = true: the hard list, resolving ties with cmp_full.
+template <bool ODD, bool HARD>
+__device__ __forceinline__ int switch_vertex(const DevGame &g, int64_t v, const uint4 *cpx,
+                                             unsigned long long &reads, unsigned long long &fulls) {
+    constexpr int B = 4;
     const int32_t SINK = (int32_t)g.n_int;
-    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    unsigned long long local = 0;
-    for (int64_t v = lo + blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); v < hi; v += nwarps) {
-        int32_t cur = g.succ[v];
-        uint32_t beg = g.rp[v], end = g.rp[v + 1];
-        int32_t best = g.col[beg];
-        int32_t nc = (int32_t)(end - beg) + (ODD ? 0 : 1);
-        for (int e = 1; e < nc; e++) {
-            int32_t c = (beg + e < end) ? g.col[beg + e] : SINK;
-            int cm = cmp_wide(g, c, best, lane);
-            if (ODD ? cm < 0 : cm > 0) best = c;
+    const int32_t cur = __ldg(g.succ + v);
+    const uint32_t beg = __ldg(g.rp + v), end = __ldg(g.rp + v + 1);
+    const int32_t ncand = (int32_t)(end - beg) + (ODD ? 0 : 1);
+    int32_t best = -1;
+    uint32_t bw[8], cw[8];
+#pragma unroll
+    for (int j = 0; j < 8; j++) { bw[j] = 0; cw[j] = 0; }
+    for (int k0 = 0; k0 < ncand; k0 += B) {
+        int32_t c[B];
+        uint4 x0[B], x1[B];
+#pragma unroll
+        for (int k = 0; k < B; k++) {
+            const int e = k0 + k;
+            c[k] = -1;
+            if (e < ncand) c[k] = (beg + e < end) ? __ldg(g.col + beg + e) : SINK;
         }
-        int cm = cmp_wide(g, best, cur, lane);
-        bool sw = ODD ? cm < 0 : cm > 0;
-        if (sw && lane == 0) { g.succ[v] = best; local++; }
+#pragma unroll
+        for (int k = 0; k < B; k++) {
+            if (c[k] >= 0) {
+                x0[k] = __ldg(cpx + 2 * (int64_t)c[k]);
+                x1[k] = __ldg(cpx + 2 * (int64_t)c[k] + 1);
+                reads += (c[k] != SINK);
+            } else {
+                x0[k] = make_uint4(0, 0, 0, 0);
+                x1[k] = x0[k];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < B; k++) {
+            if (c[k] < 0) continue;
+            const uint32_t w[8] = {x0[k].x, x0[k].y, x0[k].z, x0[k].w, x1[k].x, x1[k].y, x1[k].z, x1[k].w};
+            if (c[k] == cur) {
+#pragma unroll
+                for (int j = 0; j < 8; j++) cw[j] = w[j];
+            }
+            bool take = best < 0;
+            if (!take) {
+                int r = cmp_cpx(w, bw);
+                if (r == 2) {
+                    if constexpr (!HARD) return 2;
+                    else { r = cmp_full(g, c[k], best); fulls++; }
+                }
+                take = ODD ? r < 0 : r > 0;
+            }
+            if (take) {
+                best = c[k];
+#pragma unroll
+                for (int j = 0; j < 8; j++) bw[j] = w[j];
+            }
+        }
     }
-    unsigned long long tot = block_sum(local);
-    if (threadIdx.x == 0 && tot) atomicAdd(ODD ? &g.ctl->odd_switches : &g.ctl->even_switches, tot);
+    int r = 0;
+    if (best != cur) {
+        r = cmp_cpx(bw, cw);
+        if (r == 2) {
+            if constexpr (!HARD) return 2;
+            else { r = cmp_full(g, best, cur); fulls++; }
+        }
+    }
+    if (ODD ? r < 0 : r > 0) {
+        // σ[S] / τ[S] is applied after both passes (k_apply_switches): the hard pass
+        // re-walks plays of the *current* profile, so succ must not change before it.
+        g.swl[atomicAdd(&g.ctl->nswl, 1ull)] = make_int2((int32_t)v, best);
+        return 1;
+    }
+    return 0;
+}
+
+__global__ void k_apply_switches(DevGame g) {
+    const int64_t cnt = (int64_t)__ldcg(&g.ctl->nswl);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int2 e = __ldcg(g.swl + i);
+        g.succ[e.x] = e.y;
+    }
+}
+
+template <bool ODD, bool HARD>
+__global__ void __launch_bounds__(kThreads) k_switch(DevGame g) {
+    if (__ldcg(&g.ctl->spl_overflow)) return;
+    const int64_t lo = ODD ? g.n_even : 0;
+    const int64_t hi = HARD ? (int64_t)__ldcg(&g.ctl->nhard) : (ODD ? g.n_int : g.n_even);
+    const uint4 *cpx = reinterpret_cast<const uint4 *>(g.cpx);
+    unsigned long long nsw = 0, reads = 0, fulls = 0;
+    for (int64_t i = (HARD ? 0 : lo) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hi;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = HARD ? (int64_t)__ldcg(g.hard + i) : i;
+        const int r = switch_vertex<ODD, HARD>(g, v, cpx, reads, fulls);
+        if (r == 1) nsw++;
+        if constexpr (!HARD) {
+            if (r == 2) g.hard[atomicAdd(&g.ctl->nhard, 1ull)] = (int32_t)v;
+        }
+    }
+    unsigned long long t = block_sum(nsw);
+    if (threadIdx.x == 0 && t) atomicAdd(ODD ? &g.ctl->odd_switches : &g.ctl->even_switches, t);
+    t = block_sum(reads);
+    if (threadIdx.x == 0 && t) atomicAdd(ODD ? &g.ctl->rows_odd : &g.ctl->rows_even, t);
+    if constexpr (HARD) {
+        t = block_sum(fulls);
+        if (threadIdx.x == 0 && t) atomicAdd(ODD ? &g.ctl->full_odd : &g.ctl->full_even, t);
+    }
 }
 
 // --------------------------------------------------------------------------
@@ -757,10 +855,14 @@ cudaError_t launch_splitters(const DevGame &g, const LaunchCfg &lc, cudaStream_t
     return e;
 }
 
-cudaError_t launch_v2(const DevGame &g, cudaStream_t s) {
+cudaError_t launch_v2(const DevGame &g, cudaStream_t s, bool full_rows) {
     const int nchunk = g.dp > 32 ? g.dp / 32 : 1;
+    if (!full_rows) {
+        k_v2_cpx<<<grid_for(g.n_int, kThreads, 16), kThreads, 0, s>>>(g, nchunk);
+        return cudaGetLastError();
+    }
     const int grid = grid_for((g.n_int + 31) / 32, kThreads / 32);
-#define WALK(G) k_v2_walk<G><<<grid, kThreads, 0, s>>>(g, nchunk)
+#define WALK(G) k_v2_rows<G><<<grid, kThreads, 0, s>>>(g, nchunk)
     DISPATCH_G(g.dp, WALK);
 #undef WALK
     return cudaGetLastError();
@@ -777,29 +879,19 @@ cudaError_t launch_cycle_dom(const DevGame &g, const LaunchCfg &lc, cudaStream_t
 cudaError_t launch_switch(const DevGame &g, bool odd, cudaStream_t s) {
     const int64_t nv = odd ? g.n_int - g.n_even : g.n_even;
     if (nv <= 0) return cudaSuccess;
-    if (g.dp > 128) {
-        const int grid = grid_for(nv, kThreads / 32);
-        if (odd) k_switch_wide<true><<<grid, kThreads, 0, s>>>(g);
-        else k_switch_wide<false><<<grid, kThreads, 0, s>>>(g);
-        return cudaGetLastError();
-    }
-#define SW(G, VEC)                                                               \
-    {                                                                            \
-        const int grid = grid_for((nv + 32 / G - 1) / (32 / G), kThreads / 32);  \
-        if (odd) k_switch<G, VEC, true><<<grid, kThreads, 0, s>>>(g);            \
-        else k_switch<G, VEC, false><<<grid, kThreads, 0, s>>>(g);               \
-    }
-    switch (g.dp) {
-        case 1: SW(1, 1); break;
-        case 2: SW(1, 2); break;
-        case 4: SW(1, 4); break;
-        case 8: SW(2, 4); break;
-        case 16: SW(4, 4); break;
-        case 32: SW(8, 4); break;
-        case 64: SW(16, 4); break;
-        default: SW(32, 4); break;
-    }
-#undef SW
+    cudaError_t e = cudaMemsetAsync(&g.ctl->nhard, 0, 2 * sizeof(unsigned long long), s);  // nhard, nswl
+    if (e) return e;
+    const int grid = grid_for(nv, kThreads, 8);
+    if (odd) k_switch<true, false><<<grid, kThreads, 0, s>>>(g);
+    else k_switch<false, false><<<grid, kThreads, 0, s>>>(g);
+    e = cudaGetLastError();
+    if (e) return e;
+    const int hgrid = std::max(1, g_lc.sms * 2);
+    if (odd) k_switch<true, true><<<hgrid, kThreads, 0, s>>>(g);
+    else k_switch<false, true><<<hgrid, kThreads, 0, s>>>(g);
+    e = cudaGetLastError();
+    if (e) return e;
+    k_apply_switches<<<std::max(1, g_lc.sms * 4), kThreads, 0, s>>>(g);
     return cudaGetLastError();
 }
 

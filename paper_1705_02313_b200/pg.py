@@ -39,7 +39,7 @@ class PGError(RuntimeError):
 
 class Options(C.Structure):
     _fields_ = [("flags", C.c_uint32), ("device", C.c_int32), ("stream", C.c_void_p),
-                ("splitter_k", C.c_int32), ("reserved", C.c_int32),
+                ("splitter_k", C.c_int32), ("prefix_pairs", C.c_int32),
                 ("max_inner", C.c_int64), ("max_outer", C.c_int64)]
 
 
@@ -50,7 +50,8 @@ class Stats(C.Structure):
         "gpu_launches")] + [(k, C.c_double) for k in (
             "ms_load", "ms_call", "ms_v1", "ms_v2", "ms_odd", "ms_even", "ms_other")] + [
         (k, C.c_int64) for k in ("n_v1", "n_v2", "n_odd", "n_even")] + [
-        (k, C.c_double) for k in ("bytes_v1", "bytes_v2", "bytes_odd", "bytes_even")]
+        (k, C.c_double) for k in ("bytes_v1", "bytes_v2", "bytes_odd", "bytes_even")] + [
+        ("full_compares", C.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -109,14 +110,14 @@ class Game:
     def __init__(self, n, row_ptr, col, owner, priority, *, device: int = 0, stream=None,
                  preprocess: bool = True, check: bool = False, phase_timing: bool = False,
                  device_ptrs: bool = False, splitter_k: int = 0, max_inner: int = 0,
-                 max_outer: int = 0):
+                 max_outer: int = 0, prefix_pairs: int = 0):
         L = load_library()
         self._in = (np.ascontiguousarray(row_ptr, np.int64), np.ascontiguousarray(col, np.int32),
                     np.ascontiguousarray(owner, np.uint8), np.ascontiguousarray(priority, np.int32))
         flags = ((0 if preprocess else PG_NO_PREPROCESS) | (PG_CHECK_INVARIANTS if check else 0) |
                  (PG_PHASE_TIMING if phase_timing else 0) | (PG_PTRS_ON_DEVICE if device_ptrs else 0))
-        opt = Options(flags, device, C.c_void_p(stream) if stream else None, splitter_k, 0,
-                      max_inner, max_outer)
+        opt = Options(flags, device, C.c_void_p(stream) if stream else None, splitter_k,
+                      prefix_pairs, max_inner, max_outer)
         h = C.c_void_p()
         rc = L.pg_load(int(n), *[_ptr(a) for a in self._in], C.byref(opt), C.byref(h))
         self._in = None

@@ -242,3 +242,23 @@ def test_empty_game(pg):
     G = pg.Game.from_game(g)
     res = G.solve()
     assert res.winner.shape == (0,)
+
+
+@pytest.mark.parametrize("pairs,k", [(1, 32), (2, 8), (3, 5), (1, 3)])
+def test_solve_forced_full_compares(pg, pairs, k):
+    """Shrinking the compact prefix forces many undecided comparisons through the
+    hard (re-walk) pass; small K forces splitter bases into those re-walks."""
+    for seed, (n, d) in enumerate([(20000, 16), (8000, 40), (15000, 6)]):
+        g = gi.random_game(n, d, 2, 5, 50 + seed)
+        ora = Oracle(g).solve()
+        G = pg.Game.from_game(g, prefix_pairs=pairs, splitter_k=k)
+        res = G.solve(want_val=True)
+        assert_solve_equal(res, ora, n, G.d)
+        assert res.stats["full_compares"] > 0
+
+
+def test_solve_deep_structured_small_k(pg):
+    for g in (gi.ladder(30000, 5), gi.f_deep(20000), gi.hanoi(7)):
+        ora = Oracle(g).solve()
+        G = pg.Game.from_game(g, splitter_k=4, prefix_pairs=1)
+        assert_solve_equal(G.solve(want_val=True), ora, g.n, G.d)
