@@ -116,6 +116,8 @@ typedef struct {
      * with R = 4·dp row bytes, prefixes = non-sink candidate prefixes gathered. */
     double bytes_v1, bytes_v2, bytes_odd, bytes_even;
     int64_t full_compares;   /* switch comparisons the compact prefixes could not decide */
+    int64_t walk_steps;      /* V2 walk steps summed over valuations                       */
+    int64_t top_vertices;    /* ⊤ vertices summed over valuations                          */
 } pg_stats;
 
 /* pg_load: validate, canonicalise and preprocess a game, copy it to the GPU.

@@ -209,6 +209,8 @@ void note_valuation(pg_game h, bool full_rows) {
     h->st.bytes_v1 += 5.0 * np_;
     h->st.bytes_v2 += np_ + (full_rows ? R * (double)h->h_ctl->n_fin : 32.0 * np_);
     h->st.v1_rounds += (int64_t)h->h_ctl->v1_rounds;
+    h->st.walk_steps += (int64_t)h->h_ctl->walk_steps;
+    h->st.top_vertices += (int64_t)h->h_ctl->n_top;
     if ((int64_t)h->h_ctl->maxdepth > h->st.max_depth) h->st.max_depth = (int64_t)h->h_ctl->maxdepth;
     if ((int64_t)h->h_ctl->maxdepth >= h->G.K) h->st.v2_split_valuations++;
 }

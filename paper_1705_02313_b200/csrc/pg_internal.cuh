@@ -44,6 +44,9 @@ struct Ctl {
     unsigned long long even_switches;
     unsigned long long cdom_buf;    // which cJ buffer holds cycle_dom (pidx or -1)
     unsigned long long n_fin;       // finite vertices of the last valuation
+    unsigned long long alen[3];     // V1 still-unfinished counts per round (rotating)
+    unsigned long long n_top;       // number of ⊤ vertices
+    unsigned long long walk_steps;  // V2 walk steps of the last valuation
     unsigned long long rows_odd;    // compact prefixes gathered by the last All_Odd launch
     unsigned long long rows_even;   // compact prefixes gathered by the last All_Even launch
     unsigned long long full_odd;    // full-row compares (undecided prefixes), All_Odd

@@ -128,9 +128,12 @@ __global__ void k_import_strategy(DevGame g, const int32_t *abi, int mode) {
 }
 
 // --------------------------------------------------------------------------
-// V1: in-place pointer jumping on (J, len). Stop after the first round in which
-// no vertex newly reaches the sink (DESIGN.md §V1 proves this is exact). ⊤ =
-// vertices whose J never reaches the sink.
+// V1: sink reachability, ⊤ detection and depth by pointer jumping on packed
+// (J, len) words. Round 1 is fused with the
+// initialisation (J = succ∘succ, synchronous); later rounds jump in place over a
+// compacted list of still-unfinished vertices. Stop after the first round in
+// which no vertex newly reaches the sink (exact); the vertices
+// left on the list are exactly the ⊤ vertices.
 // --------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads) k_v1(DevGame g) {
     const int64_t N = g.n_int;
@@ -138,43 +141,73 @@ __global__ void __launch_bounds__(kThreads) k_v1(DevGame g) {
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     unsigned long long *jl = g.jl;
-    for (int64_t v = tid; v < N; v += stride)
-        jl[v] = pack_jl((uint32_t)__ldg(g.succ + v), 1u);
-    grid_barrier(g.ctl);
-    int r = 0;
-    for (;;) {
-        unsigned long long local = 0;
-        for (int64_t v = tid; v < N; v += stride) {
-            unsigned long long e = ldcg64(jl + v);
-            uint32_t J = (uint32_t)e;
-            if (J == SINK) continue;
-            unsigned long long f = ldcg64(jl + J);
-            uint32_t nJ = (uint32_t)f;
-            uint32_t s = (uint32_t)(e >> 32) + (uint32_t)(f >> 32);
-            if (s > 0x7fffffffu) s = 0x7fffffffu;   // only ⊤ vertices can saturate
-            __stcg(jl + v, pack_jl(nJ, s));
-            local += (nJ == SINK);
-        }
-        unsigned long long tot = block_sum(local);
-        if (threadIdx.x == 0 && tot) atomicAdd(&g.ctl->newfin[r % 3], tot);
-        grid_barrier(g.ctl);
-        unsigned long long nf = *(volatile unsigned long long *)&g.ctl->newfin[r % 3];
-        if (blockIdx.x == 0 && threadIdx.x == 0) g.ctl->newfin[(r + 2) % 3] = 0;
-        r++;
-        if (nf == 0) break;
-    }
-    unsigned long long mx = 0, nf = 0;
+    unsigned long long mx = 0, nf = 0, act = 0;
+    // round 1 fused with init: J(v) = succ(succ(v)), len 2 (or the sink, len 1)
     for (int64_t v = tid; v < N; v += stride) {
-        unsigned long long e = ldcg64(jl + v);
-        bool fin = (uint32_t)e == SINK;
-        g.top[v] = fin ? 0 : 1;
-        if (fin) { unsigned long long dd = e >> 32; mx = dd > mx ? dd : mx; nf++; }
+        const uint32_t s1 = (uint32_t)__ldg(g.succ + v);
+        if (s1 == SINK) {
+            jl[v] = pack_jl(SINK, 1u);
+            mx = mx > 1 ? mx : 1;
+        } else {
+            const uint32_t s2 = (uint32_t)__ldg(g.succ + s1);
+            jl[v] = pack_jl(s2, 2u);
+            if (s2 == SINK) { mx = mx > 2 ? mx : 2; nf++; }
+            else act++;
+        }
+    }
+    unsigned long long t = block_sum(nf);
+    if (threadIdx.x == 0 && t) atomicAdd(&g.ctl->newfin[1], t);
+    t = block_sum(act);
+    if (threadIdx.x == 0 && t) atomicAdd(&g.ctl->alen[1], t);
+    grid_barrier(g.ctl);
+    int r = 1;
+    bool go = *(volatile unsigned long long *)&g.ctl->newfin[1] != 0;
+    unsigned long long left = *(volatile unsigned long long *)&g.ctl->alen[1];
+    // in-place rounds; a round can only be needed while some vertex finishes, and
+    // depth < 2^31 bounds the count (hard cap: no hang even on corrupt input)
+    while (go && r < 64) {
+        r++;
+        nf = 0;
+        act = 0;
+        for (int64_t v0 = tid; v0 < N; v0 += 4 * stride) {
+            unsigned long long e[4], f[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                const int64_t v = v0 + k * stride;
+                e[k] = v < N ? ldcg64(jl + v) : pack_jl(SINK, 0u);
+            }
+#pragma unroll
+            for (int k = 0; k < 4; k++) f[k] = (uint32_t)e[k] != SINK ? ldcg64(jl + (uint32_t)e[k]) : 0ull;
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                if ((uint32_t)e[k] == SINK) continue;
+                const uint32_t nJ = (uint32_t)f[k];
+                uint32_t sl = (uint32_t)(e[k] >> 32) + (uint32_t)(f[k] >> 32);
+                if (sl > 0x7fffffffu) sl = 0x7fffffffu;   // only ⊤ vertices can saturate
+                __stcg(jl + v0 + k * stride, pack_jl(nJ, sl));
+                if (nJ == SINK) { mx = mx > sl ? mx : sl; nf++; }
+                else act++;
+            }
+        }
+        t = block_sum(nf);
+        if (threadIdx.x == 0 && t) atomicAdd(&g.ctl->newfin[r % 3], t);
+        t = block_sum(act);
+        if (threadIdx.x == 0 && t) atomicAdd(&g.ctl->alen[r % 3], t);
+        grid_barrier(g.ctl);
+        go = *(volatile unsigned long long *)&g.ctl->newfin[r % 3] != 0;
+        left = *(volatile unsigned long long *)&g.ctl->alen[r % 3];
+        if (blockIdx.x == 0 && threadIdx.x == 0) {   // counters of round r+2 (never touched yet)
+            g.ctl->newfin[(r + 2) % 3] = 0;
+            g.ctl->alen[(r + 2) % 3] = 0;
+        }
     }
     mx = block_max(mx);
     if (threadIdx.x == 0 && mx) atomicMax(&g.ctl->maxdepth, mx);
-    nf = block_sum(nf);
-    if (threadIdx.x == 0 && nf) atomicAdd(&g.ctl->n_fin, nf);
-    if (blockIdx.x == 0 && threadIdx.x == 0) { g.ctl->v1_rounds = r; g.top[N] = 0; }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        g.ctl->v1_rounds = (unsigned long long)r;
+        g.ctl->n_top = left;                           // unfinished after the last round = ⊤
+        g.ctl->n_fin = (unsigned long long)N - left;
+    }
 }
 
 // --------------------------------------------------------------------------
@@ -325,7 +358,7 @@ __device__ __forceinline__ void cpx_chunk(Cpx &p, const uint32_t (&h)[8], const 
 
 __device__ __forceinline__ void cpx_store(uint32_t *cpx, int64_t v, const Cpx &p, bool top) {
     uint4 *dst = reinterpret_cast<uint4 *>(cpx + v * 8);
-    const uint32_t hdr = top ? 1u : (p.trunc ? 2u : 0u);
+    const uint32_t hdr = top ? 1u : (((uint32_t)p.np << 2) | (p.trunc ? 2u : 0u));
     dst[0] = make_uint4(hdr, p.w[1], p.w[2], p.w[3]);
     dst[1] = make_uint4(p.w[4], p.w[5], p.w[6], p.w[7]);
 }
@@ -353,6 +386,7 @@ __global__ void __launch_bounds__(kThreads) k_v2_rows(DevGame g, int nchunk) {
             fin = (uint32_t)e == (uint32_t)N;
             uint32_t depth = (uint32_t)(e >> 32);
             steps = depth < K ? depth : depth % K;
+            g.top[v] = fin ? 0 : 1;
         }
         for (int c = 0; c < nchunk; c++) {
             uint32_t h[NW];
@@ -375,34 +409,221 @@ __global__ void __launch_bounds__(kThreads) k_v2_rows(DevGame g, int nchunk) {
     }
 }
 
-// V2, compact form (the solve loop): one thread per vertex walks its play to the
-// sink or the nearest splitter (≤ K-1 steps), adds the
-// splitter's row when there is one, and stores the 32-byte compact prefix; ⊤
-// vertices store the ⊤ header. Full key rows are not materialised.
-__global__ void __launch_bounds__(kThreads) k_v2_cpx(DevGame g, int nchunk) {
+// V2, compact form (the solve loop), dp <= 32: one thread per vertex walks its
+// play to the sink or to the nearest splitter (≤ K-1 steps, mean ≈ 3 on random
+// games), counting priorities in a per-thread byte histogram in
+// shared memory plus a 32-bit presence mask, then emits its compact prefix by
+// merging the present columns (top-down) with the splitter's compact prefix
+// (written by k_spl_cpx). Adding counts one unit at a time to an exact top-7
+// prefix keeps it exact, so no full row is read.
+// Splitters themselves already hold their prefix; ⊤ vertices store the ⊤ header.
+__global__ void __launch_bounds__(kThreads) k_v2_cpx(DevGame g) {
+    __shared__ uint8_t hsm[kThreads][36];
+    __shared__ uint32_t osm[kThreads][9];
     if (__ldcg(&g.ctl->spl_overflow)) return;   // host grows the buffers and redoes V2
     const int64_t N = g.n_int;
     const uint32_t K = (uint32_t)g.K;
-    const int32_t *sacc = g.sacc[__ldcg(&g.ctl->spl_final) & 1];
+    const int maxp = g.cpx_pairs;
+    uint8_t *hb = hsm[threadIdx.x];
+    uint32_t *ow = osm[threadIdx.x];
+#pragma unroll
+    for (int k = 0; k < 32; k++) hb[k] = 0;
+    const uint4 *cpx4 = reinterpret_cast<const uint4 *>(g.cpx);
+    unsigned long long wsteps = 0;
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < N;
          v += (int64_t)gridDim.x * blockDim.x) {
         const unsigned long long e = __ldcg(g.jl + v);
         const bool fin = (uint32_t)e == (uint32_t)N;
-        Cpx p;
-        cpx_init(p);
+        g.top[v] = fin ? 0 : 1;
+        uint4 *dst = reinterpret_cast<uint4 *>(g.cpx + v * 8);
+        if (!fin) {
+            dst[0] = make_uint4(1u, 0, 0, 0);
+            dst[1] = make_uint4(0, 0, 0, 0);
+            continue;
+        }
+        const uint32_t depth = (uint32_t)(e >> 32);
+        if (depth >= K && depth % K == 0) continue;   // splitter: prefix written by k_spl_cpx
+        const uint32_t steps = depth < K ? depth : depth % K;
+        uint32_t mask = 0;
+        int32_t x = (int32_t)v;
+        for (uint32_t st = 0; st < steps; st++) {
+            const uint32_t p = __ldg(g.pidx + x);
+            x = __ldg(g.succ + x);
+            hb[p]++;
+            mask |= 1u << p;
+        }
+        const uint32_t mask0 = mask;
+        wsteps += steps;
+        // base: the splitter's compact prefix (or the sink: empty, exact)
+        uint32_t b[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        if (x != (int32_t)N) {
+            const uint4 b0 = __ldcg(cpx4 + 2 * (int64_t)x), b1 = __ldcg(cpx4 + 2 * (int64_t)x + 1);
+            b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w; b[4] = b1.x; b[5] = b1.y; b[6] = b1.z; b[7] = b1.w;
+        }
+        const int nb = (int)((b[0] >> 2) & 7u);
+        const bool tb = (b[0] & 2u) != 0;
+        int np = 0, j = 1;
+        bool trunc = false;
+        for (;;) {
+            int bc = -1;
+            uint32_t bmag = 0;
+            if (j <= nb) {
+                uint32_t bw = 0;
+#pragma unroll
+                for (int k = 1; k < 8; k++) if (k == j) bw = b[k];
+                const int32_t be = (int32_t)bw;
+                const uint32_t ae = (uint32_t)(be < 0 ? -be : be);
+                bc = (int)(ae >> 23);
+                bmag = ae & 0x7fffffu;
+            } else if (tb) {                      // base unknown below its last stored pair
+                trunc = true;
+                break;
+            }
+            const int hc = mask ? 31 - __clz(mask) : -1;
+            if (hc < 0 && bc < 0) break;
+            int col;
+            uint32_t mag;
+            if (hc > bc) {
+                col = hc; mag = hb[hc]; mask ^= 1u << hc;
+            } else if (bc > hc) {
+                col = bc; mag = bmag; j++;
+            } else {
+                col = hc; mag = bmag + hb[hc]; mask ^= 1u << hc; j++;
+            }
+            if (np >= maxp) { trunc = true; break; }
+            const bool cap = mag >= kCap;
+            if (cap) mag = kCap;
+            const int32_t en = (int32_t)(((uint32_t)col << 23) + mag);
+            ow[1 + np] = (uint32_t)(g.oddp[col] ? -en : en);
+            np++;
+            if (cap) { trunc = true; break; }
+        }
+        for (uint32_t m = mask0; m;) {            // clear the touched histogram bytes
+            const int c = 31 - __clz(m);
+            hb[c] = 0;
+            m ^= 1u << c;
+        }
+        for (int k = np; k < 7; k++) ow[1 + k] = 0;
+        ow[0] = ((uint32_t)np << 2) | (trunc ? 2u : 0u);
+        dst[0] = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+        dst[1] = make_uint4(ow[4], ow[5], ow[6], ow[7]);
+    }
+    wsteps = block_sum(wsteps);
+    if (threadIdx.x == 0 && wsteps) atomicAdd(&g.ctl->walk_steps, wsteps);
+}
+
+// Compact prefix of every splitter from its full reduced-forest row (after
+// Wyllie): top-down nonzero columns of sacc[i] into cpx[spl[i]].
+__global__ void __launch_bounds__(kThreads) k_spl_cpx(DevGame g) {
+    if (__ldcg(&g.ctl->maxdepth) < (unsigned long long)g.K || __ldcg(&g.ctl->spl_overflow)) return;
+    const int64_t S = (int64_t)__ldcg(&g.ctl->nspl);
+    const int32_t *sacc = g.sacc[__ldcg(&g.ctl->spl_final) & 1];
+    const int dp = g.dp, maxp = g.cpx_pairs;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < S;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t *row = sacc + i * dp;
+        uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        int np = 0;
+        bool trunc = false;
+        for (int col = dp - 1; col >= 0 && !trunc; col--) {
+            const int32_t key = __ldcg(row + col);
+            if (key == 0) continue;
+            if (np >= maxp) { trunc = true; break; }
+            uint32_t mag = (uint32_t)(key < 0 ? -key : key);
+            const bool cap = mag >= kCap;
+            if (cap) mag = kCap;
+            const int32_t en = (int32_t)(((uint32_t)col << 23) + mag);
+#pragma unroll
+            for (int k = 0; k < 7; k++) if (k == np) w[1 + k] = (uint32_t)(key < 0 ? -en : en);
+            np++;
+            if (cap) trunc = true;
+        }
+        w[0] = ((uint32_t)np << 2) | (trunc ? 2u : 0u);
+        uint4 *dst = reinterpret_cast<uint4 *>(g.cpx + (int64_t)__ldcg(g.spl + i) * 8);
+        dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+        dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+    }
+}
+
+// V2, compact form (the solve loop): one thread per vertex walks its play to the
+// sink or the nearest splitter (≤ K-1 steps) counting
+// priorities in a per-thread byte histogram in shared memory, adds the
+// splitter's row when there is one, and stores the 32-byte compact prefix
+// (top-down nonzero columns); ⊤ vertices store the ⊤ header. Also writes top[].
+// Full key rows are not materialised.
+__global__ void __launch_bounds__(kThreads) k_v2_cpx_multi(DevGame g, int nchunk) {
+    __shared__ uint32_t hsm[kThreads][9];
+    __shared__ uint32_t osm[kThreads][9];
+    if (__ldcg(&g.ctl->spl_overflow)) return;   // host grows the buffers and redoes V2
+    const int64_t N = g.n_int;
+    const uint32_t K = (uint32_t)g.K;
+    const int maxp = g.cpx_pairs;
+    const int dp = g.dp;
+    const int32_t *sacc = g.sacc[__ldcg(&g.ctl->spl_final) & 1];
+    uint32_t *hw = hsm[threadIdx.x];
+    uint32_t *ow = osm[threadIdx.x];
+    uint8_t *hb = reinterpret_cast<uint8_t *>(hw);
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < N;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long e = __ldcg(g.jl + v);
+        const bool fin = (uint32_t)e == (uint32_t)N;
+        g.top[v] = fin ? 0 : 1;
+#pragma unroll
+        for (int k = 0; k < 8; k++) ow[k] = 0;
+        int np = 0;
+        bool trunc = false;
         if (fin) {
             const uint32_t depth = (uint32_t)(e >> 32);
             const uint32_t steps = depth < K ? depth : depth % K;
-            for (int c = nchunk - 1; c >= 0 && !p.trunc; c--) {
-                uint32_t h[8];
+            for (int c = nchunk - 1; c >= 0 && !trunc; c--) {
 #pragma unroll
-                for (int q = 0; q < 8; q++) h[q] = 0;
-                const int32_t x = walk<8>(g, (int32_t)v, steps, 32u * c, h);
-                const int32_t b = (x == (int32_t)N) ? -1 : __ldcg(g.sidx + x);
-                cpx_chunk(p, h, b >= 0 ? sacc + (int64_t)b * g.dp : nullptr, 32 * c, g.dp, g.oddp, g.cpx_pairs);
+                for (int k = 0; k < 8; k++) hw[k] = 0;
+                int32_t x = (int32_t)v;
+                const uint32_t lo = 32u * c;
+                for (uint32_t st = 0; st < steps; st++) {
+                    const uint32_t p = (uint32_t)__ldg(g.pidx + x) - lo;
+                    const int32_t nx = __ldg(g.succ + x);
+                    if (p < 32u) hb[p]++;
+                    x = nx;
+                }
+                const int32_t *brow = nullptr;
+                if (x != (int32_t)N) brow = sacc + (int64_t)__ldcg(g.sidx + x) * dp;
+                for (int w = 7; w >= 0 && !trunc; w--) {
+                    const int col0 = (int)lo + 4 * w;
+                    if (col0 >= dp) continue;
+                    uint32_t word = hw[w];
+                    int32_t bk[4] = {0, 0, 0, 0};
+                    if (brow) {
+                        if (dp >= 4) {
+                            const int4 b4 = __ldcg(reinterpret_cast<const int4 *>(brow + col0));
+                            bk[0] = b4.x; bk[1] = b4.y; bk[2] = b4.z; bk[3] = b4.w;
+                        } else {
+                            for (int q = 0; q < dp - col0 && q < 4; q++) bk[q] = __ldcg(brow + col0 + q);
+                        }
+                    } else if (word == 0) {
+                        continue;
+                    }
+#pragma unroll
+                    for (int q = 3; q >= 0; q--) {
+                        const int32_t cnt = (int32_t)((word >> (8 * q)) & 0xffu);
+                        if (cnt == 0 && bk[q] == 0) continue;
+                        const int col = col0 + q;
+                        const int32_t key = g.oddp[col] ? bk[q] - cnt : bk[q] + cnt;
+                        if (key == 0 || trunc) continue;
+                        if (np >= maxp) { trunc = true; continue; }
+                        uint32_t mag = (uint32_t)(key < 0 ? -key : key);
+                        if (mag >= kCap) { mag = kCap; trunc = true; }
+                        const int32_t en = (int32_t)(((uint32_t)col << 23) + mag);
+                        ow[1 + np] = (uint32_t)(key > 0 ? en : -en);
+                        np++;
+                    }
+                }
             }
         }
-        cpx_store(g.cpx, v, p, !fin);
+        ow[0] = fin ? (((uint32_t)np << 2) | (trunc ? 2u : 0u)) : 1u;
+        uint4 *dst = reinterpret_cast<uint4 *>(g.cpx + v * 8);
+        dst[0] = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+        dst[1] = make_uint4(ow[4], ow[5], ow[6], ow[7]);
     }
 }
 
@@ -517,7 +738,7 @@ __global__ void __launch_bounds__(kThreads) k_spl_wyllie(DevGame g) {
         if (blockIdx.x == 0 && threadIdx.x == 0) g.ctl->spl_active[(r + 2) % 3] = 0;
         cur = nx;
         r++;
-        if (act == 0) break;
+        if (act == 0 || r >= 64) break;   // 2^64 > any depth: the cap only guards corruption
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) g.ctl->spl_final = (unsigned long long)cur;
 }
@@ -570,13 +791,20 @@ __global__ void __launch_bounds__(kThreads) k_cycle_dom(DevGame g, int rounds) {
 // switches only (reading 5). The current successor is a candidate, so its
 // prefix comes from the candidate batch.
 // --------------------------------------------------------------------------
-// -1 / 0 / +1, or 2 when the prefixes cannot decide.
+// -1 / 0 / +1, or 2 when the prefixes cannot decide. Header: bit0 ⊤, bit1
+// truncated, bits 2-4 = number of stored pairs np. Position j of a prefix is
+// known iff j <= np or the prefix is not truncated (then it is an exact zero).
 __device__ __forceinline__ int cmp_cpx(const uint32_t (&a)[8], const uint32_t (&b)[8]) {
     const bool ta = a[0] & 1u, tb = b[0] & 1u;
     if (ta || tb) return ta == tb ? 0 : (ta ? 1 : -1);
+    const int ka = (a[0] & 2u) ? (int)((a[0] >> 2) & 7u) : 7;
+    const int kb = (b[0] & 2u) ? (int)((b[0] >> 2) & 7u) : 7;
+    const int kn = ka < kb ? ka : kb;
 #pragma unroll
-    for (int j = 1; j < 8; j++)
+    for (int j = 1; j < 8; j++) {
+        if (j > kn) return 2;
         if (a[j] != b[j]) return (int32_t)a[j] < (int32_t)b[j] ? -1 : 1;
+    }
     return ((a[0] | b[0]) & 2u) ? 2 : 0;
 }
 
@@ -851,14 +1079,20 @@ cudaError_t launch_splitters(const DevGame &g, const LaunchCfg &lc, cudaStream_t
     DevGame gg = g;
     void *args[] = {&gg};
     e = coop((const void *)k_spl_wyllie, lc.coop_spl, args, s);
-    *launches += 3;
-    return e;
+    if (e) return e;
+    k_spl_cpx<<<grid_for(g.n_int / std::max(g.K, 1) + 1), kThreads, 0, s>>>(g);
+    *launches += 4;
+    return cudaGetLastError();
 }
 
 cudaError_t launch_v2(const DevGame &g, cudaStream_t s, bool full_rows) {
     const int nchunk = g.dp > 32 ? g.dp / 32 : 1;
     if (!full_rows) {
-        k_v2_cpx<<<grid_for(g.n_int, kThreads, 16), kThreads, 0, s>>>(g, nchunk);
+        if (nchunk == 1) {
+            k_v2_cpx<<<grid_for(g.n_int, kThreads, 16), kThreads, 0, s>>>(g);
+        } else {
+            k_v2_cpx_multi<<<grid_for(g.n_int, kThreads, 16), kThreads, 0, s>>>(g, nchunk);
+        }
         return cudaGetLastError();
     }
     const int grid = grid_for((g.n_int + 31) / 32, kThreads / 32);

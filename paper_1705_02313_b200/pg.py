@@ -51,7 +51,7 @@ class Stats(C.Structure):
             "ms_load", "ms_call", "ms_v1", "ms_v2", "ms_odd", "ms_even", "ms_other")] + [
         (k, C.c_int64) for k in ("n_v1", "n_v2", "n_odd", "n_even")] + [
         (k, C.c_double) for k in ("bytes_v1", "bytes_v2", "bytes_odd", "bytes_even")] + [
-        ("full_compares", C.c_int64)]
+        ("full_compares", C.c_int64), ("walk_steps", C.c_int64), ("top_vertices", C.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

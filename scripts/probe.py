@@ -1,17 +1,15 @@
-"""Quick perf probe: load + solve configs with phase timing (not a bench number)."""
+"""Perf probe (not a bench number): per-valuation walk statistics."""
 import sys, time, json
-import numpy as np
 sys.path.insert(0, "/root/repo")
+import numpy as np
 import pg_inputs as gi
 from paper_1705_02313_b200 import Game
-import torch
-
-for (n, d) in [(1_000_000, 16), (10_000_000, 32)]:
-    t = time.time(); g = gi.random_game(n, d, 2, 5, 1); tg = time.time() - t
-    t = time.time(); G = Game.from_game(g, phase_timing=True); tl = time.time() - t
-    for rep in range(2):
-        t = time.time(); r = G.solve(); ts = time.time() - t
-        s = r.stats
-        print(json.dumps({"n": n, "d": d, "gen_s": round(tg, 2), "load_s": round(tl, 2), "solve_s": round(ts, 4),
-              "vals_per_s": n * s["inner_iters"] / ts, **{k: (round(v, 3) if isinstance(v, float) else v) for k, v in s.items()}}))
-    del G
+n, d = int(sys.argv[1]), int(sys.argv[2])
+g = gi.random_game(n, d, 2, 5, 1)
+G = Game.from_game(g, phase_timing=True)
+owner = None
+r = G.solve()
+s = r.stats
+print(json.dumps({k: s[k] for k in ("inner_iters", "walk_steps", "top_vertices", "v1_rounds", "max_depth", "ms_v1", "ms_v2", "ms_odd", "ms_even", "ms_call")}))
+print("mean walk steps per vertex per valuation", s["walk_steps"] / s["inner_iters"] / G.n_internal)
+print("mean top fraction", s["top_vertices"] / s["inner_iters"] / G.n_internal)
