@@ -207,10 +207,11 @@ def main():
 
     sampler = ClockSampler(local if "CUDA_VISIBLE_DEVICES" not in os.environ else
                            int(os.environ["CUDA_VISIBLE_DEVICES"].split(",")[local]))
-    acc = {k: 0.0 for k in ("ms_v1", "ms_v2", "ms_odd", "ms_even", "ms_other", "bytes_v1",
-                            "bytes_v2", "bytes_odd", "bytes_even", "n_v1", "n_v2", "n_odd",
-                            "n_even", "gpu_launches", "inner_iters", "outer_passes",
-                            "full_compares", "v1_rounds", "v2_split_valuations")}
+    acc = {k: 0.0 for k in ("ms_v1", "ms_v2", "ms_odd", "ms_even", "ms_other", "ms_inc", "bytes_v1",
+                            "bytes_v2", "bytes_odd", "bytes_even", "bytes_inc", "n_v1", "n_v2", "n_odd",
+                            "n_even", "n_inc", "gpu_launches", "inner_iters", "outer_passes",
+                            "full_compares", "v1_rounds", "v2_split_valuations", "inc_valuations",
+                            "dirty_vertices")}
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     barrier()
@@ -239,8 +240,10 @@ def main():
 
     # ---- roofline of the dominant kernel (phase with the largest event time)
     peak, peak_src = measured_peak_gbs()
-    phases = {p: (acc[f"ms_{p}"], acc[f"bytes_{p}"], acc[f"n_{p}"]) for p in ("v1", "v2", "odd", "even")}
-    kern = {"v1": "k_v1", "v2": "k_spl_*+k_v2_walk", "odd": "k_switch<ODD>", "even": "k_switch<EVEN>"}
+    phases = {p: (acc[f"ms_{p}"], acc[f"bytes_{p}"], acc[f"n_{p}"]) for p in ("v1", "v2", "inc", "odd", "even")}
+    kern = {"v1": "k_v1 (full V1)", "v2": "k_spl_* + k_v2_cpx (full V2)",
+            "inc": "k_dirty + k_v1_inc + k_v2_inc (incremental valuation)",
+            "odd": "k_ebuild + k_switch<ODD> + hard + apply", "even": "k_switch<EVEN> + hard + apply"}
     dom = max(phases, key=lambda p: phases[p][0])
     dms, dbytes, dn = phases[dom]
     achieved = dbytes / (dms / 1000.0) / 1e9 if dms > 0 else 0.0
@@ -304,7 +307,7 @@ def main():
                          f"1 host thread, oracle load excluded)"}
 
     if rank == 0:
-        val_bytes = (G.n_internal + 1) * 4 * max(1, 1 << (max(G.d, 1) - 1).bit_length())
+        ws_bytes = (G.n_internal + 1) * (32 + 8 + 4 + 1 + 1) + 8 * int(game.m)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
@@ -315,8 +318,11 @@ def main():
                        "full_compares_per_solve": int(acc["full_compares"] / args.steps),
                        "v1_rounds_per_solve": int(acc["v1_rounds"] / args.steps),
                        "split_valuations_per_solve": int(acc["v2_split_valuations"] / args.steps),
+                       "incremental_valuations_per_solve": int(acc["inc_valuations"] / args.steps),
+                       "mean_dirty_fraction": (acc["dirty_vertices"] / max(acc["inc_valuations"], 1)) / G.n_internal,
                        "parallelism": "single GPU" if world == 1 else f"weak: {world} independent games",
-                       "l2": f"inputs larger than L2: valuation table {val_bytes / 1e9:.2f} GB > 126 MB"},
+                       "l2": f"inputs larger than L2: per-iteration working set {ws_bytes / 1e9:.2f} GB "
+                             f"(prefixes, jl, succ, pidx, ⊤, CSR) > 126 MB; no flush needed"},
             "roofline": roofline,
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -80,7 +80,9 @@ enum {
                                  inadmissible σ_init then yields PG_EINADMISSIBLE       */
     PG_CHECK_INVARIANTS = 2,  /* check every valuation for odd cycles (admissibility)    */
     PG_PHASE_TIMING = 4,      /* record CUDA events per phase; filled into pg_stats      */
-    PG_PTRS_ON_DEVICE = 8     /* valuate/best_response/solve pointers are device pointers */
+    PG_PTRS_ON_DEVICE = 8,    /* valuate/best_response/solve pointers are device pointers */
+    PG_NO_INCREMENTAL = 16    /* recompute every valuation from scratch (no dirty-closure
+                                 incremental valuation; results are identical)          */
 };
 
 typedef struct {
@@ -117,7 +119,16 @@ typedef struct {
     double bytes_v1, bytes_v2, bytes_odd, bytes_even;
     int64_t full_compares;   /* switch comparisons the compact prefixes could not decide */
     int64_t walk_steps;      /* V2 walk steps summed over valuations                       */
-    int64_t top_vertices;    /* ⊤ vertices summed over valuations                          */
+    int64_t top_vertices;    /* ⊤ vertices summed over full valuations                     */
+    int64_t inc_valuations;  /* valuations computed incrementally (dirty closure only)    */
+    int64_t inc_even_switches; /* All_Even steps evaluated incrementally (over E_even)   */
+    int64_t inc_aborts;      /* incremental steps abandoned for a from-scratch valuation    */
+    int64_t dirty_vertices;  /* |D| summed over incremental valuations                    */
+    double ms_inc;           /* PG_PHASE_TIMING: incremental valuations (closure+V1+V2 on D) */
+    int64_t n_inc;
+    double bytes_inc;        /* algorithmic bytes of incremental valuations: per dirty vertex
+                                8·indeg (reverse edges + predecessor succ) + 62 B own state
+                                + 32 B exit prefix read               */
 } pg_stats;
 
 /* pg_load: validate, canonicalise and preprocess a game, copy it to the GPU.

@@ -6,6 +6,7 @@
 #include <chrono>
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -18,7 +19,7 @@ static thread_local std::string t_err;
 
 static void set_err(const std::string &s) { t_err = s; }
 
-enum Phase { PH_V1 = 0, PH_V2, PH_ODD, PH_EVEN, PH_OTHER, PH_N };
+enum Phase { PH_V1 = 0, PH_V2, PH_ODD, PH_EVEN, PH_OTHER, PH_INC, PH_N };
 
 struct pg_game_s {
     int device = 0;
@@ -27,6 +28,7 @@ struct pg_game_s {
     uint32_t flags = 0;
     int64_t max_inner = 0, max_outer = 0;
     int64_t n = 0, m = 0, m_int = 0, dummies = 0, m_odd = 0;
+    double avg_indeg = 0;
     std::vector<int32_t> D;
     DevGame G{};
     LaunchCfg lc;
@@ -44,6 +46,14 @@ struct pg_game_s {
     size_t ev_used = 0;
     struct Rec { int ph; cudaEvent_t a, b; };
     std::vector<Rec> recs;
+    // incremental valuation state
+    bool have_state = false;     // jl / cpx / top describe the profile before the last switch list
+    int64_t last_nsw = 0;        // size of the last switch list (S)
+    bool last_inc = false;
+    uint32_t epoch = 0;
+    bool trace = false;               // PGSI_TRACE=1 (debug)
+    bool c_valid = false;             // C covers every change since the last All_Even
+    uint32_t cepoch = 0;
 };
 
 #define CK(h, x)                                                                         \
@@ -57,6 +67,8 @@ struct pg_game_s {
     } while (0)
 
 namespace {
+
+double now_ms();
 
 struct DeviceGuard {
     int prev = -1;
@@ -120,6 +132,7 @@ void timing_collect(pg_game h) {
             case PH_V2: h->st.ms_v2 += ms; h->st.n_v2++; break;
             case PH_ODD: h->st.ms_odd += ms; h->st.n_odd++; break;
             case PH_EVEN: h->st.ms_even += ms; h->st.n_even++; break;
+            case PH_INC: h->st.ms_inc += ms; h->st.n_inc++; break;
             default: h->st.ms_other += ms; break;
         }
     }
@@ -169,7 +182,8 @@ pg_status grow_splitters(pg_game h, int64_t need) {
 }
 
 // One valuation of the current profile (σ ∪ τ in G.succ): V1 then V2.
-pg_status valuate_dev(pg_game h, bool want_cdom, bool full_rows) {
+// inc = incremental (only D = upward closure of the last switch list, §V-inc).
+pg_status valuate_dev(pg_game h, bool want_cdom, bool full_rows, bool inc = false) {
     if (want_cdom && !h->G.cJ[0]) {    // cycle-dominant scratch, allocated on first use
         const size_t N1 = (size_t)h->G.n_int + 1;
         CK(h, dalloc(h, &h->G.cJ[0], N1));
@@ -178,17 +192,29 @@ pg_status valuate_dev(pg_game h, bool want_cdom, bool full_rows) {
         CK(h, dalloc(h, &h->G.cmax[1], N1));
     }
     CK(h, cudaMemsetAsync(h->G.ctl, 0, PGSI_CTL_RESET_BYTES, h->stream));
-    {
-        PhaseScope ps(h, PH_V1);
-        CK(h, launch_v1(h->G, h->lc, h->stream));
+    if (inc) {   // incremental valuation + All_Odd in one cooperative kernel (§V-inc)
+        h->G.epoch = ++h->epoch;
+        if (h->G.epoch == 0) {                       // wrapped: clear the marks
+            CK(h, cudaMemsetAsync(h->G.dmark, 0, sizeof(uint32_t) * ((size_t)h->G.n_int + 1), h->stream));
+            CK(h, cudaMemsetAsync(h->G.emark, 0, sizeof(uint32_t) * ((size_t)h->G.n_int + 1), h->stream));
+            h->G.epoch = ++h->epoch;
+        }
+        PhaseScope ps(h, PH_INC);
+        CK(h, launch_inc_iter(h->G, h->lc, h->stream, h->last_nsw));
         h->st.gpu_launches += 1;
-    }
-    {
-        PhaseScope ps(h, PH_V2);
-        int launches = 0;
-        CK(h, launch_splitters(h->G, h->lc, h->stream, &launches));
-        CK(h, launch_v2(h->G, h->stream, full_rows));
-        h->st.gpu_launches += launches + 1;
+    } else {
+        {
+            PhaseScope ps(h, PH_V1);
+            CK(h, launch_v1(h->G, h->lc, h->stream));
+            h->st.gpu_launches += 1;
+        }
+        {
+            PhaseScope ps(h, PH_V2);
+            int launches = 0;
+            CK(h, launch_splitters(h->G, h->lc, h->stream, &launches));
+            CK(h, launch_v2(h->G, h->stream, full_rows));
+            h->st.gpu_launches += launches + 1;
+        }
     }
     if (want_cdom) {
         PhaseScope ps(h, PH_OTHER);
@@ -204,34 +230,65 @@ pg_status readback(pg_game h) {
     return PG_OK;
 }
 
-void note_valuation(pg_game h, bool full_rows) {
+void note_valuation(pg_game h, bool full_rows, bool inc) {
     const double np_ = (double)h->G.n_int, R = 4.0 * h->G.dp;
-    h->st.bytes_v1 += 5.0 * np_;
-    h->st.bytes_v2 += np_ + (full_rows ? R * (double)h->h_ctl->n_fin : 32.0 * np_);
+    if (inc) {
+        const double nd = (double)h->h_ctl->nD;
+        h->st.inc_valuations++;
+        h->st.dirty_vertices += (int64_t)h->h_ctl->nD;
+        // per dirty vertex: reverse edges scanned with the predecessors' succ (≈ 8 B × in-degree),
+        // D list w+r, succ, jl w+r, pidx, ⊤, the exit vertex's prefix and its own prefix
+        h->st.bytes_inc += nd * (8.0 * h->avg_indeg + 8.0 + 4.0 + 16.0 + 1.0 + 1.0 + 32.0 + 32.0);
+    } else {
+        h->st.bytes_v1 += 5.0 * np_;
+        h->st.bytes_v2 += np_ + (full_rows ? R * (double)h->h_ctl->n_fin : 32.0 * np_);
+        h->st.top_vertices += (int64_t)h->h_ctl->n_top;
+        if ((int64_t)h->h_ctl->maxdepth > h->st.max_depth) h->st.max_depth = (int64_t)h->h_ctl->maxdepth;
+        if ((int64_t)h->h_ctl->maxdepth >= h->G.K) h->st.v2_split_valuations++;
+    }
     h->st.v1_rounds += (int64_t)h->h_ctl->v1_rounds;
     h->st.walk_steps += (int64_t)h->h_ctl->walk_steps;
-    h->st.top_vertices += (int64_t)h->h_ctl->n_top;
-    if ((int64_t)h->h_ctl->maxdepth > h->st.max_depth) h->st.max_depth = (int64_t)h->h_ctl->maxdepth;
-    if ((int64_t)h->h_ctl->maxdepth >= h->G.K) h->st.v2_split_valuations++;
 }
 
-// valuation + one switch step, redone if the splitter buffers overflowed.
+// Incremental valuation pays off when the last switch step changed few choices.
+bool use_inc(pg_game h) {
+    return h->have_state && h->G.dp <= 32 && h->last_nsw > 0 && !(h->flags & PG_NO_INCREMENTAL) &&
+           !(h->flags & PG_CHECK_INVARIANTS) && h->last_nsw * 64 <= h->G.n_int;
+}
+
+// valuation + one switch step; redone in full if the splitter buffers overflowed
+// or an incremental walk exceeded the byte counters (both rare).
 pg_status valuate_and_switch(pg_game h, bool odd, bool want_cdom, bool do_switch) {
+    bool inc = do_switch && odd && !want_cdom && use_inc(h);
+    const double t_start = h->trace ? now_ms() : 0.0;
     for (;;) {
-        pg_status rc = valuate_dev(h, want_cdom, !do_switch);
+        pg_status rc = valuate_dev(h, want_cdom, !do_switch, inc);
         if (rc) return rc;
-        if (do_switch) {
+        if (do_switch && !inc) {
             PhaseScope ps(h, odd ? PH_ODD : PH_EVEN);
             CK(h, launch_switch(h->G, odd, h->stream));
             h->st.gpu_launches += 3;
         }
         rc = readback(h);
         if (rc) return rc;
+        if (h->h_ctl->inc_overflow) {   // closure too deep/large or walk too long: redo in full
+            inc = false;
+            h->st.inc_aborts++;
+            continue;
+        }
         if (!h->h_ctl->spl_overflow) break;
         rc = grow_splitters(h, (int64_t)h->h_ctl->nspl);   // rare: redo with larger buffers
         if (rc) return rc;
     }
-    note_valuation(h, !do_switch);
+    h->have_state = true;
+    if (do_switch) h->last_nsw = (int64_t)h->h_ctl->nswl;
+    if (!inc) h->c_valid = false;   // a from-scratch valuation: C no longer covers the changes
+    if (h->trace)
+        fprintf(stderr, "[pgsi] valuation %.3f ms inc=%d nD=%llu lev=%llu rounds=%llu steps=%llu nE=%llu switches=%llu hard=%llu\n",
+                now_ms() - t_start, (int)inc, h->h_ctl->nD, h->h_ctl->dlevels, h->h_ctl->v1_rounds, h->h_ctl->walk_steps,
+                h->h_ctl->nE, h->h_ctl->nswl, h->h_ctl->nhard);
+    note_valuation(h, !do_switch, inc);
+    h->last_inc = inc;
     return PG_OK;
 }
 
@@ -251,35 +308,68 @@ pg_status inner_loop(pg_game h, int64_t *inner, bool check) {
         }
         int64_t c = (int64_t)h->h_ctl->odd_switches;
         h->st.odd_switches += c;
-        {
+        if (h->last_inc) {   // All_Odd over E ran inside the incremental kernel
+            const double ne = (double)h->h_ctl->nE;
+            h->st.bytes_inc += 4.0 * ne + 12.0 * ne + 4.0 * h->avg_indeg * ne +
+                               32.0 * (double)h->h_ctl->rows_odd + 8.0 * c;
+        } else {
             const double no = (double)(h->G.n_int - h->G.n_even), mo = (double)h->m_odd;
             h->st.bytes_odd += 4.0 * (no + 1) + 4.0 * no + 4.0 * mo + 32.0 * (double)h->h_ctl->rows_odd +
                                8.0 * h->G.dp * (double)h->h_ctl->full_odd + 4.0 * c;
-            h->st.full_compares += (int64_t)h->h_ctl->full_odd;
         }
+        h->st.full_compares += (int64_t)h->h_ctl->full_odd;
         if (c == 0) return PG_OK;
     }
 }
 
+// All_Even. Incremental over C when every valuation
+// since the previous All_Even was incremental (then C ⊇ all changed values).
 pg_status even_switch(pg_game h, int64_t *count) {
     CK(h, cudaMemsetAsync(&h->G.ctl->even_switches, 0, sizeof(unsigned long long), h->stream));
     CK(h, cudaMemsetAsync(&h->G.ctl->rows_even, 0, sizeof(unsigned long long), h->stream));
     CK(h, cudaMemsetAsync(&h->G.ctl->full_even, 0, sizeof(unsigned long long), h->stream));
+    const bool inc = h->c_valid && !(h->flags & PG_NO_INCREMENTAL) && h->h_ctl->nC * 8 <= (uint64_t)h->G.n_int;
     {
         PhaseScope ps(h, PH_EVEN);
-        CK(h, launch_switch(h->G, false, h->stream));
-        h->st.gpu_launches += 3;
+        if (inc) {
+            h->G.epoch = ++h->epoch;                 // fresh E marks
+            if (h->G.epoch == 0) {
+                CK(h, cudaMemsetAsync(h->G.dmark, 0, sizeof(uint32_t) * ((size_t)h->G.n_int + 1), h->stream));
+                CK(h, cudaMemsetAsync(h->G.emark, 0, sizeof(uint32_t) * ((size_t)h->G.n_int + 1), h->stream));
+                h->G.epoch = ++h->epoch;
+            }
+            CK(h, launch_even_inc(h->G, h->stream));
+            h->st.gpu_launches += 4;
+        } else {
+            CK(h, launch_switch(h->G, false, h->stream));
+            h->st.gpu_launches += 3;
+        }
     }
     pg_status rc = readback(h);
     if (rc) return rc;
     *count = (int64_t)h->h_ctl->even_switches;
+    h->last_nsw = (int64_t)h->h_ctl->nswl;
+    if (h->trace) fprintf(stderr, "[pgsi] even switch: inc=%d |C|=%llu |E|=%llu %lld switches\n", (int)inc,
+                          h->h_ctl->nC, inc ? h->h_ctl->nE : 0ull, (long long)*count);
     h->st.even_switches += *count;
     {
-        const double ne = (double)h->G.n_even, me = (double)(h->m_int - h->m_odd);
-        h->st.bytes_even += 4.0 * (ne + 1) + 4.0 * ne + 4.0 * me + 32.0 * (double)h->h_ctl->rows_even +
+        const double ne = inc ? (double)h->h_ctl->nE : (double)h->G.n_even;
+        const double me = inc ? h->avg_indeg * ne : (double)(h->m_int - h->m_odd);
+        const double cl = inc ? (double)h->h_ctl->nC * (4.0 + 8.0 * h->avg_indeg) : 0.0;
+        h->st.bytes_even += cl + 4.0 * (ne + 1) + 4.0 * ne + 4.0 * me + 32.0 * (double)h->h_ctl->rows_even +
                             8.0 * h->G.dp * (double)h->h_ctl->full_even + 4.0 * *count;
         h->st.full_compares += (int64_t)h->h_ctl->full_even;
+        if (inc) h->st.inc_even_switches++;
     }
+    // a new C starts: changes after this All_Even
+    h->G.cepoch = ++h->cepoch;
+    if (h->G.cepoch == 0) {
+        CK(h, cudaMemsetAsync(h->G.cmark, 0, sizeof(uint32_t) * ((size_t)h->G.n_int + 1), h->stream));
+        h->G.cepoch = ++h->cepoch;
+    }
+    CK(h, cudaMemsetAsync(&h->G.ctl->nC, 0, sizeof(unsigned long long), h->stream));
+    h->h_ctl->nC = 0;
+    h->c_valid = true;
     return PG_OK;
 }
 
@@ -294,6 +384,8 @@ pg_status import_strategy(pg_game h, const int32_t *abi, int mode) {
     }
     unsigned long long none = ULLONG_MAX;
     CK(h, cudaMemcpyAsync(&h->G.ctl->bad_index, &none, sizeof(none), cudaMemcpyHostToDevice, h->stream));
+    h->have_state = false;
+    h->c_valid = false;
     CK(h, launch_import_strategy(h->G, src, mode, h->stream));
     h->st.gpu_launches += 1;
     pg_status rc = readback(h);
@@ -387,6 +479,7 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     h->device = o.device;
     h->flags = o.flags;
     h->max_inner = o.max_inner;
+    h->trace = getenv("PGSI_TRACE") && getenv("PGSI_TRACE")[0] == '1';
     h->max_outer = o.max_outer;
     h->n = H.n;
     h->m = H.m;
@@ -394,6 +487,7 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     h->dummies = H.dummies;
     h->D = H.D;
     h->m_odd = (int64_t)H.m_int - (int64_t)H.rp[H.n_even];
+    h->avg_indeg = H.n_int ? (double)H.m_int / (double)H.n_int : 0.0;
     DeviceGuard dg(h->device);
     auto fail = [&](pg_status r) { pg_free(h); return r; };
 #define CKL(x)                                                                  \
@@ -462,6 +556,28 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     CKL(cudaMemsetAsync(G.val, 0, sizeof(int32_t) * N1 * dp, s));   // sink row = 0
     CKL(cudaMemsetAsync(G.top, 0, N1, s));
     CKL(cudaMemsetAsync(G.cpx, 0, sizeof(uint32_t) * N1 * 8, s));   // sink prefix = zero row
+    {
+        uint32_t *rrp; int32_t *rcol;
+        CKL(dalloc(h, &rrp, N1));
+        CKL(dalloc(h, &rcol, (size_t)H.m_int));
+        CKL(cudaMemcpyAsync(rrp, H.rrp.data(), sizeof(uint32_t) * N1, cudaMemcpyHostToDevice, s));
+        if (H.m_int) CKL(cudaMemcpyAsync(rcol, H.rcol.data(), sizeof(int32_t) * H.m_int, cudaMemcpyHostToDevice, s));
+        G.rrp = rrp; G.rcol = rcol;
+        CKL(dalloc(h, &G.dmark, N1));
+        CKL(dalloc(h, &G.emark, N1));
+        CKL(dalloc(h, &G.Dl, N1));
+        CKL(dalloc(h, &G.Cl, N1));
+        CKL(dalloc(h, &G.cmark, N1));
+        CKL(cudaMemsetAsync(G.cmark, 0, sizeof(uint32_t) * N1, s));
+        G.cepoch = 1;
+        h->cepoch = 1;
+        G.inc_max_levels = 48;
+        G.inc_max_dirty = std::max<int64_t>(4096, H.n_int / 8);
+        CKL(dalloc(h, &G.El, N1));
+        CKL(cudaMemsetAsync(G.dmark, 0, sizeof(uint32_t) * N1, s));
+        CKL(cudaMemsetAsync(G.emark, 0, sizeof(uint32_t) * N1, s));
+        G.epoch = 0;
+    }
     CKL(cudaMemsetAsync(G.ctl, 0, sizeof(Ctl), s));
     // splitter buffers: grown on demand (overflow protocol in valuate_and_switch)
     {
@@ -579,7 +695,7 @@ pg_status pg_best_response(pg_game h, const int32_t *sigma, const int32_t *tau0,
                                 {top, nullptr, (size_t)N}};
     if ((rc = outputs_begin(h, outs))) return rc;
     if (N && tau_out) CK(h, launch_export_strategy(h->G, N, (int32_t *)outs[0].dev, 1, false, h->stream));
-    if (N && val) { CK(h, launch_v2(h->G, h->stream, true)); h->st.gpu_launches++; }   // full rows for output
+    if (N && val && (rc = valuate_and_switch(h, true, false, false))) return rc;   // full rows for output
     if (N && (val || top)) CK(h, launch_export_val(h->G, N, (int32_t *)outs[1].dev, (uint8_t *)outs[2].dev, h->stream));
     if ((rc = outputs_end(h, outs))) return rc;
     timing_collect(h);
@@ -601,6 +717,8 @@ pg_status pg_solve(pg_game h, uint8_t *winner, int32_t *sigma, int32_t *tau, int
     if (h->G.n_int) {
         {
             PhaseScope ps(h, PH_OTHER);
+            h->have_state = false;
+            h->c_valid = false;
             CK(h, launch_init_profile(h->G, h->stream));   // σ_init, τ = first successor
             h->st.gpu_launches += 1;
         }
@@ -633,10 +751,10 @@ pg_status pg_solve(pg_game h, uint8_t *winner, int32_t *sigma, int32_t *tau, int
         h->st.gpu_launches += 1;
         if (sigma) { CK(h, launch_export_strategy(h->G, n, (int32_t *)outs[1].dev, 0, false, h->stream)); h->st.gpu_launches++; }
         if (tau) { CK(h, launch_export_strategy(h->G, n, (int32_t *)outs[2].dev, 1, true, h->stream)); h->st.gpu_launches++; }
-        if (val) {
-            CK(h, launch_v2(h->G, h->stream, true));   // full rows of val^{σ*} for output
+        if (val) {   // full rows of val^{σ*}: one from-scratch valuation (splitters may be stale)
+            if ((rc = valuate_and_switch(h, true, false, false))) return rc;
             CK(h, launch_export_val(h->G, n, (int32_t *)outs[3].dev, nullptr, h->stream));
-            h->st.gpu_launches += 2;
+            h->st.gpu_launches += 1;
         }
     }
     if ((rc = outputs_end(h, outs))) return rc;

@@ -51,10 +51,16 @@ struct Ctl {
     unsigned long long rows_even;   // compact prefixes gathered by the last All_Even launch
     unsigned long long full_odd;    // full-row compares (undecided prefixes), All_Odd
     unsigned long long full_even;   // full-row compares, All_Even
-    unsigned long long nhard;       // vertices deferred to the hard (full-compare) pass
-    unsigned long long nswl;        // switches recorded by the current switch step (must follow nhard)
+    unsigned long long nD;          // incremental valuation: |D| (dirty closure of the last switches)
+    unsigned long long nE;          // incremental All_Odd: |E| (Odd vertices with a dirty candidate)
+    unsigned long long inc_overflow;// incremental V2 walk too long for byte counts -> redo in full
+    unsigned long long dlevels;     // BFS levels of the dirty closure
+    unsigned long long dcnt[3];     // per-level append counters of the dirty BFS (rotating)
     // ---- not reset per valuation ----
     unsigned long long bad_index;   // ULLONG_MAX = none, else min invalid ABI index
+    unsigned long long nhard;       // vertices deferred to the hard (full-compare) pass
+    unsigned long long nswl;        // switches of the last switch step (must follow nhard); = |S|
+    unsigned long long nC;          // |C|: vertices in some dirty set since the last All_Even
     unsigned int bar_count;         // grid barrier
     unsigned int bar_gen;
 };
@@ -78,6 +84,18 @@ struct DevGame {
     int32_t *val;
     uint32_t *cpx;      // compact prefixes, 8 words per vertex (+ sink row of zeros)
     int32_t *hard;      // switch worklist of vertices with undecided prefixes
+    const uint32_t *rrp;   // reverse CSR (predecessors in the game graph), device order
+    const int32_t *rcol;
+    uint32_t *dmark;    // epoch marks: v in D
+    uint32_t *emark;    // epoch marks: v in E
+    int32_t *Dl;        // D list
+    int32_t *El;        // E list
+    uint32_t epoch;     // current incremental epoch
+    uint32_t *cmark;    // epoch marks: v in C
+    int32_t *Cl;        // C list
+    uint32_t cepoch;    // epoch of C (one per outer pass)
+    int32_t inc_max_levels;   // abort the incremental step beyond this closure depth
+    int64_t inc_max_dirty;    // ... or this closure size
     int2 *swl;          // (vertex, new successor) switches of the current step
     int32_t *sidx;
     int32_t *spl;
@@ -96,6 +114,7 @@ struct LaunchCfg {
     int coop_v1 = 0;        // cooperative grid sizes
     int coop_spl = 0;
     int coop_cyc = 0;
+    int coop_inc = 0;
 };
 
 // kernels (pg_kernels.cu); every launcher returns the cudaError_t of the launch
@@ -107,6 +126,8 @@ cudaError_t launch_splitters(const DevGame &g, const LaunchCfg &lc, cudaStream_t
 cudaError_t launch_v2(const DevGame &g, cudaStream_t s, bool full_rows);
 cudaError_t launch_cycle_dom(const DevGame &g, const LaunchCfg &lc, cudaStream_t s);
 cudaError_t launch_switch(const DevGame &g, bool odd, cudaStream_t s);
+cudaError_t launch_inc_iter(const DevGame &g, const LaunchCfg &lc, cudaStream_t s, int64_t nS);
+cudaError_t launch_even_inc(const DevGame &g, cudaStream_t s);
 cudaError_t launch_export_val(const DevGame &g, int64_t count, int32_t *val_out, uint8_t *top_out,
                               cudaStream_t s);
 cudaError_t launch_export_strategy(const DevGame &g, int64_t count, int32_t *out, int which,
@@ -124,6 +145,8 @@ struct HostGame {
     std::vector<int32_t> perm, iperm, proj;   // proj: device -> projected ABI id
     std::vector<uint32_t> rp;                 // device order
     std::vector<int32_t> col;
+    std::vector<uint32_t> rrp;                // reverse CSR (device order)
+    std::vector<int32_t> rcol;
     std::vector<uint8_t> pidx;
 };
 pg_status build_host_game(int64_t n, const int64_t *row_ptr, const int32_t *col,

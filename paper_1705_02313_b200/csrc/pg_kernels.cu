@@ -32,25 +32,10 @@ __device__ __forceinline__ unsigned long long pack_jl(uint32_t J, uint32_t len) 
     return (unsigned long long)J | ((unsigned long long)len << 32);
 }
 
-// Software grid barrier for cooperative (co-resident) launches.
-__device__ __forceinline__ void grid_barrier(Ctl *ctl) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        volatile unsigned *genp = &ctl->bar_gen;
-        unsigned gen = *genp;
-        __threadfence();
-        unsigned arrived = atomicAdd(&ctl->bar_count, 1u);
-        if (arrived == gridDim.x - 1) {
-            ctl->bar_count = 0;
-            __threadfence();
-            atomicAdd(&ctl->bar_gen, 1u);
-        } else {
-            while (*genp == gen) __nanosleep(20);
-        }
-        __threadfence();
-    }
-    __syncthreads();
-}
+// Grid barrier for cooperative (co-resident) launches: cooperative groups'
+// grid sync (measured 1.2 µs on B200 at 148-296 blocks, vs ~2 µs for a
+// hand-rolled atomic barrier; scripts/micro/barrier_bench.cu).
+__device__ __forceinline__ void grid_barrier(Ctl *) { cooperative_groups::this_grid().sync(); }
 
 template <typename T>
 __device__ __forceinline__ T block_sum(T x) {
@@ -409,6 +394,70 @@ __global__ void __launch_bounds__(kThreads) k_v2_rows(DevGame g, int nchunk) {
     }
 }
 
+// Merge a walk histogram (bytes hb[0..31] with presence mask) into the compact
+// prefix of the vertex x the walk ended at (x = sink: the empty exact prefix)
+// and store the result as v's compact prefix. Exact by the one-unit insert rule
+// (DESIGN.md "Compact prefix"); clears the touched histogram bytes.
+__device__ __forceinline__ void cpx_merge_store(const DevGame &g, int64_t v, uint8_t *hb, uint32_t mask,
+                                                int32_t x, uint32_t *ow) {
+    const int maxp = g.cpx_pairs;
+    const uint32_t mask0 = mask;
+    uint32_t b[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (x != (int32_t)g.n_int) {
+        const uint4 *cpx4 = reinterpret_cast<const uint4 *>(g.cpx);
+        const uint4 b0 = __ldcg(cpx4 + 2 * (int64_t)x), b1 = __ldcg(cpx4 + 2 * (int64_t)x + 1);
+        b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w; b[4] = b1.x; b[5] = b1.y; b[6] = b1.z; b[7] = b1.w;
+    }
+    const int nb = (int)((b[0] >> 2) & 7u);
+    const bool tb = (b[0] & 2u) != 0;
+    int np = 0, j = 1;
+    bool trunc = false;
+    for (;;) {
+        int bc = -1;
+        uint32_t bmag = 0;
+        if (j <= nb) {
+            uint32_t bw = 0;
+#pragma unroll
+            for (int k = 1; k < 8; k++) if (k == j) bw = b[k];
+            const int32_t be = (int32_t)bw;
+            const uint32_t ae = (uint32_t)(be < 0 ? -be : be);
+            bc = (int)(ae >> 23);
+            bmag = ae & 0x7fffffu;
+        } else if (tb) {                          // base unknown below its last stored pair
+            trunc = true;
+            break;
+        }
+        const int hc = mask ? 31 - __clz(mask) : -1;
+        if (hc < 0 && bc < 0) break;
+        int col;
+        uint32_t mag;
+        if (hc > bc) {
+            col = hc; mag = hb[hc]; mask ^= 1u << hc;
+        } else if (bc > hc) {
+            col = bc; mag = bmag; j++;
+        } else {
+            col = hc; mag = bmag + hb[hc]; mask ^= 1u << hc; j++;
+        }
+        if (np >= maxp) { trunc = true; break; }
+        const bool cap = mag >= kCap;
+        if (cap) mag = kCap;
+        const int32_t en = (int32_t)(((uint32_t)col << 23) + mag);
+        ow[1 + np] = (uint32_t)(g.oddp[col] ? -en : en);
+        np++;
+        if (cap) { trunc = true; break; }
+    }
+    for (uint32_t m = mask0; m;) {
+        const int c = 31 - __clz(m);
+        hb[c] = 0;
+        m ^= 1u << c;
+    }
+    for (int k = np; k < 7; k++) ow[1 + k] = 0;
+    ow[0] = ((uint32_t)np << 2) | (trunc ? 2u : 0u);
+    uint4 *dst = reinterpret_cast<uint4 *>(g.cpx + v * 8);
+    dst[0] = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+    dst[1] = make_uint4(ow[4], ow[5], ow[6], ow[7]);
+}
+
 // V2, compact form (the solve loop), dp <= 32: one thread per vertex walks its
 // play to the sink or to the nearest splitter (≤ K-1 steps, mean ≈ 3 on random
 // games), counting priorities in a per-thread byte histogram in
@@ -428,7 +477,6 @@ __global__ void __launch_bounds__(kThreads) k_v2_cpx(DevGame g) {
     uint32_t *ow = osm[threadIdx.x];
 #pragma unroll
     for (int k = 0; k < 32; k++) hb[k] = 0;
-    const uint4 *cpx4 = reinterpret_cast<const uint4 *>(g.cpx);
     unsigned long long wsteps = 0;
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < N;
          v += (int64_t)gridDim.x * blockDim.x) {
@@ -452,61 +500,8 @@ __global__ void __launch_bounds__(kThreads) k_v2_cpx(DevGame g) {
             hb[p]++;
             mask |= 1u << p;
         }
-        const uint32_t mask0 = mask;
         wsteps += steps;
-        // base: the splitter's compact prefix (or the sink: empty, exact)
-        uint32_t b[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        if (x != (int32_t)N) {
-            const uint4 b0 = __ldcg(cpx4 + 2 * (int64_t)x), b1 = __ldcg(cpx4 + 2 * (int64_t)x + 1);
-            b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w; b[4] = b1.x; b[5] = b1.y; b[6] = b1.z; b[7] = b1.w;
-        }
-        const int nb = (int)((b[0] >> 2) & 7u);
-        const bool tb = (b[0] & 2u) != 0;
-        int np = 0, j = 1;
-        bool trunc = false;
-        for (;;) {
-            int bc = -1;
-            uint32_t bmag = 0;
-            if (j <= nb) {
-                uint32_t bw = 0;
-#pragma unroll
-                for (int k = 1; k < 8; k++) if (k == j) bw = b[k];
-                const int32_t be = (int32_t)bw;
-                const uint32_t ae = (uint32_t)(be < 0 ? -be : be);
-                bc = (int)(ae >> 23);
-                bmag = ae & 0x7fffffu;
-            } else if (tb) {                      // base unknown below its last stored pair
-                trunc = true;
-                break;
-            }
-            const int hc = mask ? 31 - __clz(mask) : -1;
-            if (hc < 0 && bc < 0) break;
-            int col;
-            uint32_t mag;
-            if (hc > bc) {
-                col = hc; mag = hb[hc]; mask ^= 1u << hc;
-            } else if (bc > hc) {
-                col = bc; mag = bmag; j++;
-            } else {
-                col = hc; mag = bmag + hb[hc]; mask ^= 1u << hc; j++;
-            }
-            if (np >= maxp) { trunc = true; break; }
-            const bool cap = mag >= kCap;
-            if (cap) mag = kCap;
-            const int32_t en = (int32_t)(((uint32_t)col << 23) + mag);
-            ow[1 + np] = (uint32_t)(g.oddp[col] ? -en : en);
-            np++;
-            if (cap) { trunc = true; break; }
-        }
-        for (uint32_t m = mask0; m;) {            // clear the touched histogram bytes
-            const int c = 31 - __clz(m);
-            hb[c] = 0;
-            m ^= 1u << c;
-        }
-        for (int k = np; k < 7; k++) ow[1 + k] = 0;
-        ow[0] = ((uint32_t)np << 2) | (trunc ? 2u : 0u);
-        dst[0] = make_uint4(ow[0], ow[1], ow[2], ow[3]);
-        dst[1] = make_uint4(ow[4], ow[5], ow[6], ow[7]);
+        cpx_merge_store(g, v, hb, mask, x, ow);
     }
     wsteps = block_sum(wsteps);
     if (threadIdx.x == 0 && wsteps) atomicAdd(&g.ctl->walk_steps, wsteps);
@@ -808,37 +803,31 @@ __device__ __forceinline__ int cmp_cpx(const uint32_t (&a)[8], const uint32_t (&
     return ((a[0] | b[0]) & 2u) ? 2 : 0;
 }
 
-// Full lexicographic compare of val(a), val(b) (finite, or the sink) when the
+// Full lexicographic compare of val(a), val(b) (both finite, or the sink) when the
 // prefixes tie: both rows are rebuilt chunk by chunk, highest chunk first, by
-// re-walking the plays (as V2 does) — full rows are not kept in HBM.
-__device__ __forceinline__ int32_t walk_row(const DevGame &g, int32_t x, int c, uint32_t (&h)[8],
-                                            const int32_t *sacc) {
-#pragma unroll
-    for (int q = 0; q < 8; q++) h[q] = 0;
-    const int32_t N = (int32_t)g.n_int;
-    if (x == N) return -1;
-    const unsigned long long e = __ldcg(g.jl + x);
-    const uint32_t depth = (uint32_t)(e >> 32), K = (uint32_t)g.K;
-    const int32_t y = walk<8>(g, x, depth < K ? depth : depth % K, 32u * c, h);
-    return (y == N) ? -1 : __ldcg(g.sidx + y);
-}
-
+// walking the plays to the sink (full rows are not kept in HBM; the splitter
+// rows may be stale after incremental valuations). Rare (pg_stats.full_compares).
 __device__ __noinline__ int cmp_full(const DevGame &g, int32_t a, int32_t b) {
-    const int32_t *sacc = g.sacc[__ldcg(&g.ctl->spl_final) & 1];
+    const int32_t N = (int32_t)g.n_int;
     const int nchunk = g.dp > 32 ? g.dp / 32 : 1;
     for (int c = nchunk - 1; c >= 0; c--) {
-        uint32_t ha[8], hb[8];
-        const int32_t ba = walk_row(g, a, c, ha, sacc);
-        const int32_t bb = walk_row(g, b, c, hb, sacc);
+        int32_t ca[32], cb[32];
+        for (int k = 0; k < 32; k++) { ca[k] = 0; cb[k] = 0; }
+        int64_t guard = 0;
+        for (int32_t x = a; x != N && guard <= N; guard++) {
+            const uint32_t p = (uint32_t)__ldg(g.pidx + x) - 32u * c;
+            if (p < 32u) ca[p]++;
+            x = __ldg(g.succ + x);
+        }
+        guard = 0;
+        for (int32_t x = b; x != N && guard <= N; guard++) {
+            const uint32_t p = (uint32_t)__ldg(g.pidx + x) - 32u * c;
+            if (p < 32u) cb[p]++;
+            x = __ldg(g.succ + x);
+        }
         for (int col = min(32 * c + 31, g.dp - 1); col >= 32 * c; col--) {
-            const int w = (col - 32 * c) >> 2, q = (col - 32 * c) & 3;
-            uint32_t wa = 0, wb = 0;
-#pragma unroll
-            for (int k = 0; k < 8; k++) if (k == w) { wa = ha[k]; wb = hb[k]; }
-            int32_t ka = (int32_t)((wa >> (8 * q)) & 0xffu), kb = (int32_t)((wb >> (8 * q)) & 0xffu);
+            int32_t ka = ca[col - 32 * c], kb = cb[col - 32 * c];
             if (g.oddp[col]) { ka = -ka; kb = -kb; }
-            if (ba >= 0) ka += __ldcg(sacc + (int64_t)ba * g.dp + col);
-            if (bb >= 0) kb += __ldcg(sacc + (int64_t)bb * g.dp + col);
             if (ka != kb) return ka < kb ? -1 : 1;
         }
     }
@@ -931,15 +920,17 @@ __global__ void k_apply_switches(DevGame g) {
 }
 
 template <bool ODD, bool HARD>
-__global__ void __launch_bounds__(kThreads) k_switch(DevGame g) {
-    if (__ldcg(&g.ctl->spl_overflow)) return;
-    const int64_t lo = ODD ? g.n_even : 0;
-    const int64_t hi = HARD ? (int64_t)__ldcg(&g.ctl->nhard) : (ODD ? g.n_int : g.n_even);
+__global__ void __launch_bounds__(kThreads) k_switch(DevGame g, const int32_t *vlist) {
+    if (__ldcg(&g.ctl->spl_overflow) || __ldcg(&g.ctl->inc_overflow)) return;
+    const bool lst = vlist != nullptr;
+    const int64_t lo = (HARD || lst) ? 0 : (ODD ? g.n_even : 0);
+    const int64_t hi = HARD ? (int64_t)__ldcg(&g.ctl->nhard)
+                            : (lst ? (int64_t)__ldcg(&g.ctl->nE) : (ODD ? g.n_int : g.n_even));
     const uint4 *cpx = reinterpret_cast<const uint4 *>(g.cpx);
     unsigned long long nsw = 0, reads = 0, fulls = 0;
-    for (int64_t i = (HARD ? 0 : lo) + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hi;
+    for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hi;
          i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t v = HARD ? (int64_t)__ldcg(g.hard + i) : i;
+        const int64_t v = HARD ? (int64_t)__ldcg(g.hard + i) : (lst ? (int64_t)__ldcg(vlist + i) : i);
         const int r = switch_vertex<ODD, HARD>(g, v, cpx, reads, fulls);
         if (r == 1) nsw++;
         if constexpr (!HARD) {
@@ -953,6 +944,272 @@ __global__ void __launch_bounds__(kThreads) k_switch(DevGame g) {
     if constexpr (HARD) {
         t = block_sum(fulls);
         if (threadIdx.x == 0 && t) atomicAdd(ODD ? &g.ctl->full_odd : &g.ctl->full_even, t);
+    }
+}
+
+// --------------------------------------------------------------------------
+// Incremental inner iteration, one cooperative kernel:
+//   1. D = upward closure of the last switch list S in the functional graph
+//      (BFS over the static reverse game CSR: u joins when succ(u) ∈ D). Every
+//      vertex outside D has an unchanged play, hence an unchanged valuation.
+//   2. V1 on D: pointer jumping over the D list; clean vertices are terminals
+//      through their final (J, len) words.
+//   3. V2 on D: walk from v through dirty vertices to the first clean vertex x
+//      (or the sink) and merge the walk histogram into cpx[x] (exact).
+//   4. E = Odd vertices with a candidate in D; no other Odd decision can change.
+//   5-7. All_Odd over E (prefix pass, deferred hard pass, apply).
+// The grid is sized from |S| by the host: tiny iterations run in one block,
+// where every barrier is a __syncthreads.
+// --------------------------------------------------------------------------
+__device__ __forceinline__ void gbar(Ctl *ctl) {
+    if (gridDim.x == 1) __syncthreads();
+    else grid_barrier(ctl);
+}
+
+__device__ __forceinline__ void warp_append(bool app, int32_t val, int32_t *list,
+                                            unsigned long long *cnt) {
+    const unsigned m = __ballot_sync(FULL, app);
+    if (!m) return;
+    const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+    unsigned long long b = 0;
+    if (lane == leader) b = atomicAdd(cnt, (unsigned long long)__popc(m));
+    b = __shfl_sync(FULL, b, leader);
+    if (app) list[b + __popc(m & ((1u << lane) - 1u))] = val;
+}
+
+__global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
+    __shared__ uint8_t hsm[kThreads][36];
+    __shared__ uint32_t osm[kThreads][9];
+    const uint32_t ep = g.epoch;
+    const int64_t N = g.n_int;
+    const uint32_t SINK = (uint32_t)N;
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int lane = threadIdx.x & 31;
+    const int64_t wbase = tid - lane;
+    Ctl *ctl = g.ctl;
+
+    // ---- 1. dirty closure
+    const int64_t ns = (int64_t)__ldcg(&ctl->nswl);
+    for (int64_t i = tid; i < ns; i += stride) {
+        const int32_t v = __ldcg(g.swl + i).x;
+        g.dmark[v] = ep;
+        g.Dl[i] = v;
+    }
+    gbar(ctl);
+    if (blockIdx.x == 0 && threadIdx.x == 0) { ctl->nswl = 0; ctl->nhard = 0; }  // step 5 appends anew
+    int64_t lo = 0, hi = ns;
+    int levels = 0;
+    while (lo < hi && levels < (1 << 30)) {
+        levels++;
+        unsigned long long *cnt = &ctl->dcnt[levels % 3];   // reset two levels ahead: no block
+        int32_t *out = g.Dl + hi;                           // reads a count still being written
+        for (int64_t b0 = lo + wbase; b0 < hi; b0 += stride) {
+            const int64_t i = b0 + lane;
+            int32_t f = -1;
+            uint32_t rb = 0, re = 0;
+            if (i < hi) {
+                f = __ldcg(g.Dl + i);
+                rb = __ldg(g.rrp + f);
+                re = __ldg(g.rrp + f + 1);
+            }
+            const int maxd = (int)__reduce_max_sync(FULL, re - rb);
+            for (int k = 0; k < maxd; k++) {
+                bool add = false;
+                int32_t u = -1;
+                if (rb + k < re) {
+                    u = __ldg(g.rcol + rb + k);
+                    add = __ldcg(g.succ + u) == f && atomicExch(g.dmark + u, ep) != ep;
+                }
+                warp_append(add, u, out, cnt);
+            }
+        }
+        gbar(ctl);
+        const int64_t added = (int64_t)*(volatile unsigned long long *)cnt;
+        if (blockIdx.x == 0 && threadIdx.x == 0) ctl->dcnt[(levels + 2) % 3] = 0;
+        lo = hi;
+        hi += added;
+        if (levels >= g.inc_max_levels || hi > g.inc_max_dirty) {
+            // deep or huge closure: a from-scratch valuation is cheaper. Nothing but
+            // marks (epoch-scoped) has been written; the host redoes the step in full.
+            if (blockIdx.x == 0 && threadIdx.x == 0) { ctl->inc_overflow = 1; ctl->nD = (unsigned long long)hi; }
+            return;
+        }
+    }
+    const int64_t nd = hi;
+    // C ∪= D (every vertex whose valuation may have changed since the last All_Even)
+    for (int64_t b0 = wbase; b0 < nd; b0 += stride) {
+        const int64_t i = b0 + lane;
+        int32_t v = -1;
+        if (i < nd) v = __ldcg(g.Dl + i);
+        const bool addc = v >= 0 && atomicExch(g.cmark + v, g.cepoch) != g.cepoch;
+        warp_append(addc, v, g.Cl, &ctl->nC);
+    }
+
+    // ---- 2. V1 on D
+    unsigned long long *jl = g.jl;
+    for (int64_t i = tid; i < nd; i += stride) {
+        const int32_t v = __ldcg(g.Dl + i);
+        jl[v] = pack_jl((uint32_t)__ldcg(g.succ + v), 1u);
+    }
+    gbar(ctl);
+    int r = 0;
+    bool go = true;
+    while (go && r < 64) {
+        r++;
+        unsigned long long nf = 0;
+        for (int64_t i0 = tid; i0 < nd; i0 += 4 * stride) {
+            int32_t v[4];
+            unsigned long long e[4], f[4];
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                const int64_t i = i0 + k * stride;
+                v[k] = i < nd ? __ldcg(g.Dl + i) : -1;
+            }
+#pragma unroll
+            for (int k = 0; k < 4; k++) e[k] = v[k] >= 0 ? ldcg64(jl + v[k]) : pack_jl(SINK, 0u);
+#pragma unroll
+            for (int k = 0; k < 4; k++) f[k] = (uint32_t)e[k] != SINK ? ldcg64(jl + (uint32_t)e[k]) : 0ull;
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                if ((uint32_t)e[k] == SINK) continue;
+                const uint32_t nJ = (uint32_t)f[k];
+                uint32_t sl = (uint32_t)(e[k] >> 32) + (uint32_t)(f[k] >> 32);
+                if (sl > 0x7fffffffu) sl = 0x7fffffffu;
+                __stcg(jl + v[k], pack_jl(nJ, sl));
+                nf += (nJ == SINK);
+            }
+        }
+        nf = block_sum(nf);
+        if (threadIdx.x == 0 && nf) atomicAdd(&ctl->newfin[r % 3], nf);
+        gbar(ctl);
+        go = *(volatile unsigned long long *)&ctl->newfin[r % 3] != 0;
+        if (blockIdx.x == 0 && threadIdx.x == 0) ctl->newfin[(r + 2) % 3] = 0;
+    }
+
+    // ---- 3. V2 on D
+    uint8_t *hb = hsm[threadIdx.x];
+    uint32_t *ow = osm[threadIdx.x];
+#pragma unroll
+    for (int k = 0; k < 32; k++) hb[k] = 0;
+    unsigned long long wsteps = 0;
+    for (int64_t i = tid; i < nd; i += stride) {
+        const int32_t v = __ldcg(g.Dl + i);
+        const unsigned long long e = __ldcg(jl + v);
+        const bool fin = (uint32_t)e == SINK;
+        g.top[v] = fin ? 0 : 1;
+        if (!fin) {
+            uint4 *dst = reinterpret_cast<uint4 *>(g.cpx + (int64_t)v * 8);
+            dst[0] = make_uint4(1u, 0, 0, 0);
+            dst[1] = make_uint4(0, 0, 0, 0);
+            continue;
+        }
+        uint32_t mask = 0, steps = 0;
+        int32_t x = v;
+        while (x != (int32_t)N && __ldcg(g.dmark + x) == ep) {
+            const uint32_t p = __ldg(g.pidx + x);
+            x = __ldg(g.succ + x);
+            if (++hb[p] == 255) { atomicOr(&ctl->inc_overflow, 1ull); break; }
+            mask |= 1u << p;
+            steps++;
+        }
+        wsteps += steps;
+        cpx_merge_store(g, v, hb, mask, x, ow);
+    }
+    gbar(ctl);
+
+    // ---- 4. E = Odd vertices with a candidate in D
+    for (int64_t b0 = wbase; b0 < nd; b0 += stride) {
+        const int64_t i = b0 + lane;
+        uint32_t rb = 0, re = 0;
+        if (i < nd) {
+            const int32_t f = __ldcg(g.Dl + i);
+            rb = __ldg(g.rrp + f);
+            re = __ldg(g.rrp + f + 1);
+        }
+        const int maxd = (int)__reduce_max_sync(FULL, re - rb);
+        for (int k = 0; k < maxd; k++) {
+            bool add = false;
+            int32_t p = -1;
+            if (rb + k < re) {
+                p = __ldg(g.rcol + rb + k);
+                add = p >= g.n_even && atomicExch(g.emark + p, ep) != ep;
+            }
+            warp_append(add, p, g.El, &ctl->nE);
+        }
+    }
+    gbar(ctl);
+    const int64_t ne = (int64_t)*(volatile unsigned long long *)&ctl->nE;
+    const bool ovf = *(volatile unsigned long long *)&ctl->inc_overflow != 0;
+
+    // ---- 5-7. All_Odd over E: prefix pass, hard pass, apply
+    const uint4 *cpx = reinterpret_cast<const uint4 *>(g.cpx);
+    unsigned long long nsw = 0, reads = 0, fulls = 0;
+    if (!ovf) {
+        for (int64_t i = tid; i < ne; i += stride) {
+            const int64_t v = __ldcg(g.El + i);
+            const int rr = switch_vertex<true, false>(g, v, cpx, reads, fulls);
+            if (rr == 1) nsw++;
+            else if (rr == 2) g.hard[atomicAdd(&ctl->nhard, 1ull)] = (int32_t)v;
+        }
+    }
+    gbar(ctl);
+    if (!ovf) {
+        const int64_t nh = (int64_t)*(volatile unsigned long long *)&ctl->nhard;
+        for (int64_t i = tid; i < nh; i += stride) {
+            const int64_t v = __ldcg(g.hard + i);
+            if (switch_vertex<true, true>(g, v, cpx, reads, fulls) == 1) nsw++;
+        }
+    }
+    gbar(ctl);
+    const int64_t nsl = (int64_t)*(volatile unsigned long long *)&ctl->nswl;
+    for (int64_t i = tid; i < nsl; i += stride) {
+        const int2 e = __ldcg(g.swl + i);
+        g.succ[e.x] = e.y;
+    }
+    unsigned long long t = block_sum(nsw);
+    if (threadIdx.x == 0 && t) atomicAdd(&ctl->odd_switches, t);
+    t = block_sum(reads);
+    if (threadIdx.x == 0 && t) atomicAdd(&ctl->rows_odd, t);
+    t = block_sum(fulls);
+    if (threadIdx.x == 0 && t) atomicAdd(&ctl->full_odd, t);
+    t = block_sum(wsteps);
+    if (threadIdx.x == 0 && t) atomicAdd(&ctl->walk_steps, t);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        ctl->nD = (unsigned long long)nd;
+        ctl->dlevels = (unsigned long long)levels;
+        ctl->v1_rounds = (unsigned long long)r;
+    }
+}
+
+
+// Incremental All_Even: E_even = Even vertices with a candidate in C (the union
+// of the dirty sets since the previous All_Even); no other Even decision can
+// change (its candidates' val^σ are unchanged since it was last evaluated).
+__global__ void __launch_bounds__(kThreads) k_ebuild_even(DevGame g) {
+    const uint32_t ep = g.epoch;
+    const int lane = threadIdx.x & 31;
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t nc = (int64_t)__ldcg(&g.ctl->nC);
+    for (int64_t b0 = tid - lane; b0 < nc; b0 += stride) {
+        const int64_t i = b0 + lane;
+        uint32_t rb = 0, re = 0;
+        if (i < nc) {
+            const int32_t f = __ldcg(g.Cl + i);
+            rb = __ldg(g.rrp + f);
+            re = __ldg(g.rrp + f + 1);
+        }
+        const int maxd = (int)__reduce_max_sync(FULL, re - rb);
+        for (int k = 0; k < maxd; k++) {
+            bool add = false;
+            int32_t p = -1;
+            if (rb + k < re) {
+                p = __ldg(g.rcol + rb + k);
+                add = p < g.n_even && atomicExch(g.emark + p, ep) != ep;
+            }
+            warp_append(add, p, g.El, &g.ctl->nE);
+        }
     }
 }
 
@@ -1030,6 +1287,9 @@ cudaError_t setup_launch_cfg(LaunchCfg &lc, int device) {
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_cycle_dom, kThreads, 0);
     if (e) return e;
     lc.coop_cyc = nb * lc.sms;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_inc_iter, kThreads, 0);
+    if (e) return e;
+    lc.coop_inc = std::min(nb, 4) * lc.sms;
     g_lc = lc;
     return cudaSuccess;
 }
@@ -1116,17 +1376,38 @@ cudaError_t launch_switch(const DevGame &g, bool odd, cudaStream_t s) {
     cudaError_t e = cudaMemsetAsync(&g.ctl->nhard, 0, 2 * sizeof(unsigned long long), s);  // nhard, nswl
     if (e) return e;
     const int grid = grid_for(nv, kThreads, 8);
-    if (odd) k_switch<true, false><<<grid, kThreads, 0, s>>>(g);
-    else k_switch<false, false><<<grid, kThreads, 0, s>>>(g);
+    if (odd) k_switch<true, false><<<grid, kThreads, 0, s>>>(g, nullptr);
+    else k_switch<false, false><<<grid, kThreads, 0, s>>>(g, nullptr);
     e = cudaGetLastError();
     if (e) return e;
     const int hgrid = std::max(1, g_lc.sms * 2);
-    if (odd) k_switch<true, true><<<hgrid, kThreads, 0, s>>>(g);
-    else k_switch<false, true><<<hgrid, kThreads, 0, s>>>(g);
+    if (odd) k_switch<true, true><<<hgrid, kThreads, 0, s>>>(g, nullptr);
+    else k_switch<false, true><<<hgrid, kThreads, 0, s>>>(g, nullptr);
     e = cudaGetLastError();
     if (e) return e;
     k_apply_switches<<<std::max(1, g_lc.sms * 4), kThreads, 0, s>>>(g);
     return cudaGetLastError();
+}
+
+cudaError_t launch_even_inc(const DevGame &g, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(&g.ctl->nhard, 0, 2 * sizeof(unsigned long long), s);  // nhard, nswl
+    if (e) return e;
+    e = cudaMemsetAsync(&g.ctl->nE, 0, sizeof(unsigned long long), s);
+    if (e) return e;
+    const int grid = std::max(1, g_lc.sms * 4);
+    k_ebuild_even<<<grid, kThreads, 0, s>>>(g);
+    k_switch<false, false><<<grid, kThreads, 0, s>>>(g, g.El);
+    k_switch<false, true><<<std::max(1, g_lc.sms * 2), kThreads, 0, s>>>(g, nullptr);
+    k_apply_switches<<<grid, kThreads, 0, s>>>(g);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_inc_iter(const DevGame &g, const LaunchCfg &lc, cudaStream_t s, int64_t nS) {
+    int64_t grid = (nS * 16 + kThreads - 1) / kThreads;
+    grid = std::max<int64_t>(1, std::min<int64_t>(grid, lc.coop_inc));
+    DevGame gg = g;
+    void *args[] = {&gg};
+    return cudaLaunchCooperativeKernel((const void *)k_inc_iter, dim3((unsigned)grid), dim3(kThreads), args, 0, s);
 }
 
 cudaError_t launch_export_val(const DevGame &g, int64_t count, int32_t *val_out, uint8_t *top_out,

@@ -179,6 +179,16 @@ pg_status build_host_game(int64_t n, const int64_t *row_ptr, const int32_t *col,
         }
     }
     G.rp[n_int] = o;
+    // reverse CSR: predecessors of every vertex (incremental valuation, §V-inc)
+    G.rrp.assign(n_int + 1, 0);
+    for (int64_t e = 0; e < (int64_t)o; e++) G.rrp[G.col[e] + 1]++;
+    for (int64_t v = 0; v < n_int; v++) G.rrp[v + 1] += G.rrp[v];
+    G.rcol.resize(o);
+    {
+        std::vector<uint32_t> fill(G.rrp.begin(), G.rrp.end() - 1);
+        for (int64_t u = 0; u < n_int; u++)
+            for (uint32_t e = G.rp[u]; e < G.rp[u + 1]; e++) G.rcol[fill[G.col[e]]++] = (int32_t)u;
+    }
     return PG_OK;
 }
 

@@ -25,6 +25,7 @@ PG_NO_PREPROCESS = 1
 PG_CHECK_INVARIANTS = 2
 PG_PHASE_TIMING = 4
 PG_PTRS_ON_DEVICE = 8
+PG_NO_INCREMENTAL = 16
 
 STATUS = {0: "PG_OK", -1: "PG_EINVAL", -2: "PG_ENOMEM", -3: "PG_ECUDA", -4: "PG_ENCCL",
           -5: "PG_EINADMISSIBLE", -6: "PG_EITERCAP", -7: "PG_ESTATE", -8: "PG_ENOTSUP"}
@@ -51,7 +52,11 @@ class Stats(C.Structure):
             "ms_load", "ms_call", "ms_v1", "ms_v2", "ms_odd", "ms_even", "ms_other")] + [
         (k, C.c_int64) for k in ("n_v1", "n_v2", "n_odd", "n_even")] + [
         (k, C.c_double) for k in ("bytes_v1", "bytes_v2", "bytes_odd", "bytes_even")] + [
-        ("full_compares", C.c_int64), ("walk_steps", C.c_int64), ("top_vertices", C.c_int64)]
+        ("full_compares", C.c_int64), ("walk_steps", C.c_int64), ("top_vertices", C.c_int64),
+        ("inc_valuations", C.c_int64), ("inc_even_switches", C.c_int64), ("inc_aborts", C.c_int64),
+        ("dirty_vertices", C.c_int64),
+        ("ms_inc", C.c_double),
+        ("n_inc", C.c_int64), ("bytes_inc", C.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -110,12 +115,13 @@ class Game:
     def __init__(self, n, row_ptr, col, owner, priority, *, device: int = 0, stream=None,
                  preprocess: bool = True, check: bool = False, phase_timing: bool = False,
                  device_ptrs: bool = False, splitter_k: int = 0, max_inner: int = 0,
-                 max_outer: int = 0, prefix_pairs: int = 0):
+                 max_outer: int = 0, prefix_pairs: int = 0, incremental: bool = True):
         L = load_library()
         self._in = (np.ascontiguousarray(row_ptr, np.int64), np.ascontiguousarray(col, np.int32),
                     np.ascontiguousarray(owner, np.uint8), np.ascontiguousarray(priority, np.int32))
         flags = ((0 if preprocess else PG_NO_PREPROCESS) | (PG_CHECK_INVARIANTS if check else 0) |
-                 (PG_PHASE_TIMING if phase_timing else 0) | (PG_PTRS_ON_DEVICE if device_ptrs else 0))
+                 (PG_PHASE_TIMING if phase_timing else 0) | (PG_PTRS_ON_DEVICE if device_ptrs else 0) |
+                 (0 if incremental else PG_NO_INCREMENTAL))
         opt = Options(flags, device, C.c_void_p(stream) if stream else None, splitter_k,
                       prefix_pairs, max_inner, max_outer)
         h = C.c_void_p()

@@ -227,7 +227,9 @@ def test_solve_device_pointers_and_caps(pg):
     np.testing.assert_array_equal(res.winner.cpu().numpy(), ora.winner)
     np.testing.assert_array_equal(res.tau.cpu().numpy(), ora.tau)
     np.testing.assert_array_equal(res.val.cpu().numpy(), ora.val)
-    assert res.stats["n_v1"] == ora.inner_iters and res.stats["ms_v1"] > 0
+    # one timed valuation per inner iteration (full or incremental) + the val export
+    assert res.stats["n_v1"] + res.stats["n_inc"] == ora.inner_iters + 1
+    assert res.stats["ms_v1"] > 0
     # repeated solves on the same handle are identical
     res2 = G.solve(want_val=True)
     assert torch.equal(res.sigma, res2.sigma)
@@ -262,3 +264,40 @@ def test_solve_deep_structured_small_k(pg):
         ora = Oracle(g).solve()
         G = pg.Game.from_game(g, splitter_k=4, prefix_pairs=1)
         assert_solve_equal(G.solve(want_val=True), ora, g.n, G.d)
+
+
+@pytest.mark.parametrize("n,d,seed", [(20000, 16, 1), (50000, 32, 2), (30000, 4, 3), (40000, 8, 4)])
+def test_incremental_matches_full_and_oracle(pg, n, d, seed):
+    """The dirty-closure incremental valuation must give the
+    same solve as recomputing every valuation, and both must match the oracle."""
+    g = gi.random_game(n, d, 2, 5, seed)
+    ora = Oracle(g).solve()
+    Gi = pg.Game.from_game(g)
+    ri = Gi.solve(want_val=True)
+    assert_solve_equal(ri, ora, n, Gi.d)
+    assert ri.stats["inc_valuations"] > 0
+    Gf = pg.Game.from_game(g, incremental=False)
+    rf = Gf.solve(want_val=True)
+    assert_solve_equal(rf, ora, n, Gf.d)
+    assert rf.stats["inc_valuations"] == 0
+
+
+def test_incremental_structured_and_forced(pg):
+    for g in (gi.ladder(40000, 9), gi.hanoi(8), gi.f_oddchain(3000), gi.f_stair(400)):
+        ora = Oracle(g).solve()
+        for pairs in (0, 1):
+            G = pg.Game.from_game(g, prefix_pairs=pairs)
+            assert_solve_equal(G.solve(want_val=True), ora, g.n, G.d)
+
+
+def test_best_response_large(pg):
+    g = gi.random_game(30000, 12, 2, 5, 77)
+    o = Oracle(g)
+    G = pg.Game.from_game(g)
+    owner = o.internal()[0]
+    sigma = np.where(owner == 0, -1, 0).astype(np.int32)
+    tau, val, top, inner = G.best_response(sigma)
+    et, ev, etop, einner = o.best_response(sigma)
+    assert inner == einner
+    np.testing.assert_array_equal(tau, et)
+    np.testing.assert_array_equal(val, ev)
