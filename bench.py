@@ -257,6 +257,34 @@ def main():
                                "GBps": (v[1] / (v[0] / 1000.0) / 1e9) if v[0] else None,
                                "launches": int(v[2] / args.steps)} for p, v in phases.items()}}
 
+    # ---- the same solve with every valuation recomputed from scratch (no §V-inc)
+    scratch = None
+    if not args.profile:
+        Gs = Game.from_game(game, device=local, stream=stream.cuda_stream, device_ptrs=True,
+                            incremental=False)
+        for _ in range(2):
+            Gs.solve(out=out)
+        barrier()
+        torch.cuda.synchronize(dev)
+        e0.record(stream)
+        s_units = 0.0
+        for _ in range(args.steps):
+            rs = Gs.solve(out=out)
+            s_units += float(n) * rs.stats["inner_iters"]
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        sms = e0.elapsed_time(e1)
+        if dist is not None:
+            t = torch.tensor([sms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            sms = float(t.item())
+            u = torch.tensor([s_units], device=dev, dtype=torch.float64)
+            dist.all_reduce(u, op=dist.ReduceOp.SUM)
+            s_units = float(u.item())
+        scratch = {"value": s_units / (sms / 1000.0), "ms_per_step": sms / args.steps,
+                   "note": "PG_NO_INCREMENTAL: every valuation recomputed for all vertices"}
+        Gs.free()
+
     # ---- end to end through the public API, pinned host buffers
     e2e = None
     if not args.no_e2e and not args.profile:
@@ -324,6 +352,7 @@ def main():
                        "l2": f"inputs larger than L2: per-iteration working set {ws_bytes / 1e9:.2f} GB "
                              f"(prefixes, jl, succ, pidx, ⊤, CSR) > 126 MB; no flush needed"},
             "roofline": roofline,
+            "from_scratch": scratch,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": sampler.summary(),
