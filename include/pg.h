@@ -81,8 +81,10 @@ enum {
     PG_CHECK_INVARIANTS = 2,  /* check every valuation for odd cycles (admissibility)    */
     PG_PHASE_TIMING = 4,      /* record CUDA events per phase; filled into pg_stats      */
     PG_PTRS_ON_DEVICE = 8,    /* valuate/best_response/solve pointers are device pointers */
-    PG_NO_INCREMENTAL = 16    /* recompute every valuation from scratch (no dirty-closure
+    PG_NO_INCREMENTAL = 16,   /* recompute every valuation from scratch (no dirty-closure
                                  incremental valuation; results are identical)          */
+    PG_HOST_LOAD = 32         /* run pg_load's transform on the host (pg_load.cpp) instead
+                                 of the GPU (pg_load_dev.cu); results are identical      */
 };
 
 typedef struct {

@@ -470,10 +470,7 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     double t0 = now_ms();
     pg_options o{};
     if (opt) o = *opt;
-    HostGame H;
-    std::string err;
-    pg_status rc = build_host_game(n, row_ptr, col, owner, priority, !(o.flags & PG_NO_PREPROCESS), H, err);
-    if (rc) { set_err(err); return rc; }
+    const bool preprocess = !(o.flags & PG_NO_PREPROCESS);
 
     pg_game h = new pg_game_s();
     h->device = o.device;
@@ -481,13 +478,6 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     h->max_inner = o.max_inner;
     h->trace = getenv("PGSI_TRACE") && getenv("PGSI_TRACE")[0] == '1';
     h->max_outer = o.max_outer;
-    h->n = H.n;
-    h->m = H.m;
-    h->m_int = H.m_int;
-    h->dummies = H.dummies;
-    h->D = H.D;
-    h->m_odd = (int64_t)H.m_int - (int64_t)H.rp[H.n_even];
-    h->avg_indeg = H.n_int ? (double)H.m_int / (double)H.n_int : 0.0;
     DeviceGuard dg(h->device);
     auto fail = [&](pg_status r) { pg_free(h); return r; };
 #define CKL(x)                                                                  \
@@ -506,24 +496,77 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
         h->own_stream = true;
     }
     CKL(setup_launch_cfg(h->lc, h->device));
-
+    cudaStream_t s = h->stream;
     DevGame &G = h->G;
-    G.n_int = H.n_int;
-    G.n_even = H.n_even;
-    G.d = H.d;
+
+    // ---- §8(a1) load-time transform: on the GPU (default) or on the host
+    DevLoadOut L;
+    std::string err;
+    if (o.flags & PG_HOST_LOAD) {
+        HostGame H;
+        pg_status rc = build_host_game(n, row_ptr, col, owner, priority, preprocess, H, err);
+        if (rc) { set_err(err); return fail(rc); }
+        const size_t N1 = (size_t)H.n_int + 1;
+        uint32_t *rp, *rrp; int32_t *colp, *rcol, *perm, *iperm, *proj; uint8_t *pidx;
+        CKL(dalloc(h, &rp, N1));
+        CKL(dalloc(h, &colp, (size_t)H.m_int));
+        CKL(dalloc(h, &pidx, N1));
+        CKL(dalloc(h, &perm, (size_t)H.n_int));
+        CKL(dalloc(h, &iperm, (size_t)H.n_int));
+        CKL(dalloc(h, &proj, (size_t)H.n_int));
+        CKL(dalloc(h, &rrp, N1));
+        CKL(dalloc(h, &rcol, (size_t)H.m_int));
+        CKL(cudaMemcpyAsync(rp, H.rp.data(), sizeof(uint32_t) * N1, cudaMemcpyHostToDevice, s));
+        if (H.m_int) CKL(cudaMemcpyAsync(colp, H.col.data(), sizeof(int32_t) * H.m_int, cudaMemcpyHostToDevice, s));
+        CKL(cudaMemcpyAsync(pidx, H.pidx.data(), N1, cudaMemcpyHostToDevice, s));
+        CKL(cudaMemcpyAsync(rrp, H.rrp.data(), sizeof(uint32_t) * N1, cudaMemcpyHostToDevice, s));
+        if (H.m_int) CKL(cudaMemcpyAsync(rcol, H.rcol.data(), sizeof(int32_t) * H.m_int, cudaMemcpyHostToDevice, s));
+        if (H.n_int) {
+            CKL(cudaMemcpyAsync(perm, H.perm.data(), sizeof(int32_t) * H.n_int, cudaMemcpyHostToDevice, s));
+            CKL(cudaMemcpyAsync(iperm, H.iperm.data(), sizeof(int32_t) * H.n_int, cudaMemcpyHostToDevice, s));
+            CKL(cudaMemcpyAsync(proj, H.proj.data(), sizeof(int32_t) * H.n_int, cudaMemcpyHostToDevice, s));
+        }
+        CKL(cudaStreamSynchronize(s));   // H's vectors go out of scope
+        L.n_int = H.n_int; L.n_even = H.n_even; L.m_int = H.m_int; L.m = H.m; L.dummies = H.dummies;
+        L.d = H.d; L.D = H.D; L.rp = rp; L.col = colp; L.pidx = pidx; L.perm = perm; L.iperm = iperm;
+        L.proj = proj; L.rrp = rrp; L.rcol = rcol;
+        L.m_odd = (int64_t)H.m_int - (int64_t)H.rp[H.n_even];
+    } else {
+        auto persist = [h](size_t bytes) -> void * {
+            void *p = nullptr;
+            if (cudaMalloc(&p, std::max<size_t>(bytes, 16)) != cudaSuccess) return nullptr;
+            h->allocs.push_back(p);
+            return p;
+        };
+        pg_status rc = build_device_game(n, row_ptr, col, owner, priority, preprocess, s, persist, L, err);
+        if (rc) { set_err(err); return fail(rc); }
+        uint32_t rpe = 0;
+        CKL(cudaMemcpy(&rpe, L.rp + L.n_even, 4, cudaMemcpyDeviceToHost));
+        L.m_odd = (int64_t)L.m_int - (int64_t)rpe;
+    }
+    h->n = n;
+    h->m = L.m;
+    h->m_int = L.m_int;
+    h->dummies = L.dummies;
+    h->D = L.D;
+    h->m_odd = L.m_odd;
+    h->avg_indeg = L.n_int ? (double)L.m_int / (double)L.n_int : 0.0;
+    G.n_int = L.n_int;
+    G.n_even = L.n_even;
+    G.d = L.d;
+    G.rp = L.rp; G.col = L.col; G.pidx = L.pidx;
+    G.perm = L.perm; G.iperm = L.iperm; G.proj = L.proj;
+    G.rrp = L.rrp; G.rcol = L.rcol;
     int dp = 1;                          // row width: pow2 up to 128, else multiple of 32
-    if (H.d <= 128) { while (dp < H.d) dp <<= 1; }
-    else dp = (H.d + 31) / 32 * 32;
+    if (L.d <= 128) { while (dp < L.d) dp <<= 1; }
+    else dp = (L.d + 31) / 32 * 32;
     G.dp = dp;
     G.K = o.splitter_k > 0 ? std::min(o.splitter_k, 255) : 32;
     G.cpx_pairs = (o.prefix_pairs >= 1 && o.prefix_pairs <= 7) ? o.prefix_pairs : 7;
-    const size_t N1 = (size_t)H.n_int + 1;
-    uint32_t *rp; int32_t *colp; uint8_t *pidx, *oddp;
-    int32_t *perm, *iperm, *proj;
-    CKL(dalloc(h, &rp, N1));
-    CKL(dalloc(h, &colp, (size_t)H.m_int));
-    CKL(dalloc(h, &pidx, N1));
+    const size_t N1 = (size_t)L.n_int + 1;
+    uint8_t *oddp;
     CKL(dalloc(h, &oddp, (size_t)std::max(dp, 32)));
+    G.oddp = oddp;
     CKL(dalloc(h, &G.succ, N1));
     CKL(dalloc(h, &G.jl, N1));
     CKL(dalloc(h, &G.top, N1));
@@ -532,56 +575,35 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     CKL(dalloc(h, &G.hard, N1));
     CKL(dalloc(h, &G.swl, N1));
     CKL(dalloc(h, &G.sidx, N1));
-    CKL(dalloc(h, &perm, (size_t)H.n_int));
-    CKL(dalloc(h, &iperm, (size_t)H.n_int));
-    CKL(dalloc(h, &proj, (size_t)H.n_int));
     CKL(dalloc(h, &G.ctl, 1));
-    CKL(dalloc(h, &h->d_D, (size_t)std::max(1, H.d)));
+    CKL(dalloc(h, &h->d_D, (size_t)std::max(1, L.d)));
     CKL(cudaMallocHost((void **)&h->h_ctl, sizeof(Ctl)));
-    G.rp = rp; G.col = colp; G.pidx = pidx; G.oddp = oddp;
-    G.perm = perm; G.iperm = iperm; G.proj = proj;
     std::vector<uint8_t> odd(std::max(dp, 32), 0);
-    for (int i = 0; i < H.d; i++) odd[i] = (uint8_t)(H.D[i] & 1);
-    cudaStream_t s = h->stream;
-    CKL(cudaMemcpyAsync(rp, H.rp.data(), sizeof(uint32_t) * N1, cudaMemcpyHostToDevice, s));
-    if (H.m_int) CKL(cudaMemcpyAsync(colp, H.col.data(), sizeof(int32_t) * H.m_int, cudaMemcpyHostToDevice, s));
-    CKL(cudaMemcpyAsync(pidx, H.pidx.data(), N1, cudaMemcpyHostToDevice, s));
+    for (int i = 0; i < L.d; i++) odd[i] = (uint8_t)(L.D[i] & 1);
     CKL(cudaMemcpyAsync(oddp, odd.data(), odd.size(), cudaMemcpyHostToDevice, s));
-    if (H.n_int) {
-        CKL(cudaMemcpyAsync(perm, H.perm.data(), sizeof(int32_t) * H.n_int, cudaMemcpyHostToDevice, s));
-        CKL(cudaMemcpyAsync(iperm, H.iperm.data(), sizeof(int32_t) * H.n_int, cudaMemcpyHostToDevice, s));
-        CKL(cudaMemcpyAsync(proj, H.proj.data(), sizeof(int32_t) * H.n_int, cudaMemcpyHostToDevice, s));
-    }
-    if (H.d) CKL(cudaMemcpyAsync(h->d_D, H.D.data(), sizeof(int32_t) * H.d, cudaMemcpyHostToDevice, s));
+    if (L.d) CKL(cudaMemcpyAsync(h->d_D, L.D.data(), sizeof(int32_t) * L.d, cudaMemcpyHostToDevice, s));
     CKL(cudaMemsetAsync(G.val, 0, sizeof(int32_t) * N1 * dp, s));   // sink row = 0
     CKL(cudaMemsetAsync(G.top, 0, N1, s));
     CKL(cudaMemsetAsync(G.cpx, 0, sizeof(uint32_t) * N1 * 8, s));   // sink prefix = zero row
-    {
-        uint32_t *rrp; int32_t *rcol;
-        CKL(dalloc(h, &rrp, N1));
-        CKL(dalloc(h, &rcol, (size_t)H.m_int));
-        CKL(cudaMemcpyAsync(rrp, H.rrp.data(), sizeof(uint32_t) * N1, cudaMemcpyHostToDevice, s));
-        if (H.m_int) CKL(cudaMemcpyAsync(rcol, H.rcol.data(), sizeof(int32_t) * H.m_int, cudaMemcpyHostToDevice, s));
-        G.rrp = rrp; G.rcol = rcol;
-        CKL(dalloc(h, &G.dmark, N1));
-        CKL(dalloc(h, &G.emark, N1));
-        CKL(dalloc(h, &G.Dl, N1));
-        CKL(dalloc(h, &G.Cl, N1));
-        CKL(dalloc(h, &G.cmark, N1));
-        CKL(cudaMemsetAsync(G.cmark, 0, sizeof(uint32_t) * N1, s));
-        G.cepoch = 1;
-        h->cepoch = 1;
-        G.inc_max_levels = 48;
-        G.inc_max_dirty = std::max<int64_t>(4096, H.n_int / 8);
-        CKL(dalloc(h, &G.El, N1));
-        CKL(cudaMemsetAsync(G.dmark, 0, sizeof(uint32_t) * N1, s));
-        CKL(cudaMemsetAsync(G.emark, 0, sizeof(uint32_t) * N1, s));
-        G.epoch = 0;
-    }
+    // incremental-valuation state (§V-inc)
+    CKL(dalloc(h, &G.dmark, N1));
+    CKL(dalloc(h, &G.emark, N1));
+    CKL(dalloc(h, &G.cmark, N1));
+    CKL(dalloc(h, &G.Dl, N1));
+    CKL(dalloc(h, &G.El, N1));
+    CKL(dalloc(h, &G.Cl, N1));
+    CKL(cudaMemsetAsync(G.dmark, 0, sizeof(uint32_t) * N1, s));
+    CKL(cudaMemsetAsync(G.emark, 0, sizeof(uint32_t) * N1, s));
+    CKL(cudaMemsetAsync(G.cmark, 0, sizeof(uint32_t) * N1, s));
+    G.epoch = 0;
+    G.cepoch = 1;
+    h->cepoch = 1;
+    G.inc_max_levels = 48;
+    G.inc_max_dirty = std::max<int64_t>(4096, L.n_int / 8);
     CKL(cudaMemsetAsync(G.ctl, 0, sizeof(Ctl), s));
     // splitter buffers: grown on demand (overflow protocol in valuate_and_switch)
     {
-        int64_t cap = std::min<int64_t>(H.n_int + 1, H.n_int / G.K + 4096);
+        int64_t cap = std::min<int64_t>(L.n_int + 1, L.n_int / G.K + 4096);
         CKL(dalloc(h, &G.spl, (size_t)cap));
         CKL(dalloc(h, &G.sJ[0], (size_t)cap));
         CKL(dalloc(h, &G.sJ[1], (size_t)cap));
@@ -592,12 +614,12 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     CKL(launch_init_profile(G, s));
     CKL(cudaStreamSynchronize(s));
 #undef CKL
-    h->st.n = H.n;
-    h->st.n_internal = H.n_int;
-    h->st.m = H.m;
-    h->st.m_internal = H.m_int;
-    h->st.d = H.d;
-    h->st.dummies = H.dummies;
+    h->st.n = n;
+    h->st.n_internal = L.n_int;
+    h->st.m = L.m;
+    h->st.m_internal = L.m_int;
+    h->st.d = L.d;
+    h->st.dummies = L.dummies;
     h->st.ms_load = now_ms() - t0;
     *out = h;
     return PG_OK;

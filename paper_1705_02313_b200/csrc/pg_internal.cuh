@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 #include <stddef.h>
 #include <stdint.h>
+#include <functional>
 #include <string>
 #include <vector>
 
@@ -149,6 +150,19 @@ struct HostGame {
     std::vector<int32_t> rcol;
     std::vector<uint8_t> pidx;
 };
+// device-side load transform (pg_load_dev.cu)
+struct DevLoadOut {
+    int64_t n_int = 0, n_even = 0, m_int = 0, m = 0, dummies = 0, m_odd = 0;
+    int32_t d = 0;
+    std::vector<int32_t> D;
+    uint32_t *rp = nullptr, *rrp = nullptr;
+    int32_t *col = nullptr, *rcol = nullptr, *perm = nullptr, *iperm = nullptr, *proj = nullptr;
+    uint8_t *pidx = nullptr;
+};
+pg_status build_device_game(int64_t n, const int64_t *row_ptr, const int32_t *col, const uint8_t *owner,
+                            const int32_t *priority, bool preprocess, cudaStream_t s,
+                            const std::function<void *(size_t)> &persist, DevLoadOut &out, std::string &err);
+
 pg_status build_host_game(int64_t n, const int64_t *row_ptr, const int32_t *col,
                           const uint8_t *owner, const int32_t *priority, bool preprocess,
                           HostGame &out, std::string &err);

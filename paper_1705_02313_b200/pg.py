@@ -26,6 +26,7 @@ PG_CHECK_INVARIANTS = 2
 PG_PHASE_TIMING = 4
 PG_PTRS_ON_DEVICE = 8
 PG_NO_INCREMENTAL = 16
+PG_HOST_LOAD = 32
 
 STATUS = {0: "PG_OK", -1: "PG_EINVAL", -2: "PG_ENOMEM", -3: "PG_ECUDA", -4: "PG_ENCCL",
           -5: "PG_EINADMISSIBLE", -6: "PG_EITERCAP", -7: "PG_ESTATE", -8: "PG_ENOTSUP"}
@@ -115,13 +116,14 @@ class Game:
     def __init__(self, n, row_ptr, col, owner, priority, *, device: int = 0, stream=None,
                  preprocess: bool = True, check: bool = False, phase_timing: bool = False,
                  device_ptrs: bool = False, splitter_k: int = 0, max_inner: int = 0,
-                 max_outer: int = 0, prefix_pairs: int = 0, incremental: bool = True):
+                 max_outer: int = 0, prefix_pairs: int = 0, incremental: bool = True,
+                 host_load: bool = False):
         L = load_library()
         self._in = (np.ascontiguousarray(row_ptr, np.int64), np.ascontiguousarray(col, np.int32),
                     np.ascontiguousarray(owner, np.uint8), np.ascontiguousarray(priority, np.int32))
         flags = ((0 if preprocess else PG_NO_PREPROCESS) | (PG_CHECK_INVARIANTS if check else 0) |
                  (PG_PHASE_TIMING if phase_timing else 0) | (PG_PTRS_ON_DEVICE if device_ptrs else 0) |
-                 (0 if incremental else PG_NO_INCREMENTAL))
+                 (0 if incremental else PG_NO_INCREMENTAL) | (PG_HOST_LOAD if host_load else 0))
         opt = Options(flags, device, C.c_void_p(stream) if stream else None, splitter_k,
                       prefix_pairs, max_inner, max_outer)
         h = C.c_void_p()

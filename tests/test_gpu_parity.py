@@ -301,3 +301,57 @@ def test_best_response_large(pg):
     assert inner == einner
     np.testing.assert_array_equal(tau, et)
     np.testing.assert_array_equal(val, ev)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_device_load_matches_host_load(pg, seed):
+    """§8(a1) on the GPU (pg_load_dev.cu) vs the host transform (PG_HOST_LOAD):
+    same internal game, hence identical valuations of the same ABI profile and
+    identical solves (tie-breaks depend on the canonical adjacency order)."""
+    rng = np.random.default_rng(400 + seed)
+    n = int(rng.integers(1, 30000))
+    g = gi.random_game(n, int(rng.integers(1, 40)), 1, int(rng.integers(1, 7)), seed)
+    Gd = pg.Game.from_game(g)
+    Gh = pg.Game.from_game(g, host_load=True)
+    assert (Gd.n_internal, Gd.d, Gd.dummies) == (Gh.n_internal, Gh.d, Gh.dummies)
+    assert list(Gd.priorities) == list(Gh.priorities)
+    o = Oracle(g)
+    s = random_profile(o, rng, 0.2)
+    vd = Gd.valuate(s)
+    vh = Gh.valuate(s)
+    for a, b in zip(vd, vh):
+        np.testing.assert_array_equal(a, b)
+    rd, rh = Gd.solve(want_val=True), Gh.solve(want_val=True)
+    for k in ("winner", "sigma", "tau", "val"):
+        np.testing.assert_array_equal(getattr(rd, k), getattr(rh, k))
+    assert rd.stats["inner_iters"] == rh.stats["inner_iters"]
+
+
+def test_device_load_structured_and_duplicates(pg):
+    for g in (gi.ladder(20000, 4), gi.hanoi(7), gi.f_deep(3000), gi.f_oddchain(500),
+              gi.from_adjacency([1, 1, 0, 1], [5, 0, 2, 3], [[2, 1, 1, 0, 3, 3], [0, 1], [2, 2], [3]])):
+        ora = Oracle(g).solve()
+        G = pg.Game.from_game(g)
+        assert_solve_equal(G.solve(want_val=True), ora, g.n, G.d)
+
+
+@pytest.mark.parametrize("bad", ["terminal", "range", "owner", "priority"])
+def test_device_load_errors_match_host(pg, bad):
+    g = gi.random_game(200, 4, 1, 3, 9)
+    if bad == "terminal":
+        adj = [g.successors(v) for v in range(g.n)]
+        adj[57] = []
+        g = gi.from_adjacency(g.owner, g.priority, adj)
+    elif bad == "range":
+        g.col[31] = 999
+    elif bad == "owner":
+        g.owner[44] = 2
+    else:
+        g.priority[90] = -1
+    msgs = []
+    for host in (False, True):
+        with pytest.raises(pg.PGError) as e:
+            pg.Game.from_game(g, host_load=host)
+        assert e.value.name == "PG_EINVAL"
+        msgs.append(str(e.value))
+    assert msgs[0] == msgs[1]
