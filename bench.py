@@ -322,7 +322,7 @@ def main():
             ems, e_units = float(t[0].item()), float(tt[1].item())
         e2e = {"value": e_units / (ems / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": ems / e2e_steps, "steps": e2e_steps,
-               "includes": "pg_load (validate, canonicalise, preprocess on host; H2D) + pg_solve + D2H"}
+               "includes": "pg_load (H2D of the raw CSR, then validate / canonicalise / preprocess / reorder on the GPU) + pg_solve + D2H of winner, sigma, tau"}
 
     # ---- CPU oracle baseline (rank 0, N = 1 only)
     cpu = None

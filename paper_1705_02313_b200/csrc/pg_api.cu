@@ -83,18 +83,29 @@ struct DeviceGuard {
     }
 };
 
+// Handle memory comes from the device's stream-ordered pool, kept cached across
+// handles (release threshold = max), so repeated pg_load / pg_free cycles (e2e)
+// do not pay cudaMalloc/cudaFree each time.
 template <typename T>
 cudaError_t dalloc(pg_game h, T **p, size_t count) {
     size_t bytes = std::max<size_t>(count * sizeof(T), 16);
-    cudaError_t e = cudaMalloc((void **)p, bytes);
+    cudaError_t e = cudaMallocAsync((void **)p, bytes, h->stream);
     if (e == cudaSuccess) h->allocs.push_back((void *)*p);
     return e;
 }
 
 void dfree(pg_game h, void *p) {
     if (!p) return;
-    cudaFree(p);
+    cudaFreeAsync(p, h->stream);
     h->allocs.erase(std::remove(h->allocs.begin(), h->allocs.end(), p), h->allocs.end());
+}
+
+cudaError_t keep_pool_cached(int device) {
+    cudaMemPool_t pool;
+    cudaError_t e = cudaDeviceGetDefaultMemPool(&pool, device);
+    if (e) return e;
+    uint64_t thr = UINT64_MAX;
+    return cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
 }
 
 cudaEvent_t ev_get(pg_game h) {
@@ -159,7 +170,7 @@ pg_status grow_staging(pg_game h, void **buf, size_t *cap, size_t need) {
     if (*buf) dfree(h, *buf);
     *buf = nullptr;
     *cap = 0;
-    CK(h, cudaMalloc(buf, need));
+    CK(h, cudaMallocAsync(buf, need, h->stream));
     h->allocs.push_back(*buf);
     *cap = need;
     return PG_OK;
@@ -184,6 +195,11 @@ pg_status grow_splitters(pg_game h, int64_t need) {
 // One valuation of the current profile (σ ∪ τ in G.succ): V1 then V2.
 // inc = incremental (only D = upward closure of the last switch list, §V-inc).
 pg_status valuate_dev(pg_game h, bool want_cdom, bool full_rows, bool inc = false) {
+    if (full_rows && !h->G.val) {   // full key rows are only needed for outputs: allocated lazily
+        const size_t N1 = (size_t)h->G.n_int + 1;
+        CK(h, dalloc(h, &h->G.val, N1 * h->G.dp));
+        CK(h, cudaMemsetAsync(h->G.val, 0, sizeof(int32_t) * N1 * h->G.dp, h->stream));   // sink row = 0
+    }
     if (want_cdom && !h->G.cJ[0]) {    // cycle-dominant scratch, allocated on first use
         const size_t N1 = (size_t)h->G.n_int + 1;
         CK(h, dalloc(h, &h->G.cJ[0], N1));
@@ -455,8 +471,11 @@ const char *pg_version(void) { return "pgsi-b200 0.1 (sm_100a)"; }
 void pg_free(pg_game h) {
     if (!h) return;
     DeviceGuard dg(h->device);
+    for (void *p : h->allocs) {
+        if (h->stream) cudaFreeAsync(p, h->stream);
+        else cudaFree(p);
+    }
     if (h->stream) cudaStreamSynchronize(h->stream);
-    for (void *p : h->allocs) cudaFree(p);
     if (h->h_ctl) cudaFreeHost(h->h_ctl);
     for (auto e : h->ev_pool) cudaEventDestroy(e);
     if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
@@ -496,6 +515,7 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
         h->own_stream = true;
     }
     CKL(setup_launch_cfg(h->lc, h->device));
+    CKL(keep_pool_cached(h->device));
     cudaStream_t s = h->stream;
     DevGame &G = h->G;
 
@@ -534,7 +554,7 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     } else {
         auto persist = [h](size_t bytes) -> void * {
             void *p = nullptr;
-            if (cudaMalloc(&p, std::max<size_t>(bytes, 16)) != cudaSuccess) return nullptr;
+            if (cudaMallocAsync(&p, std::max<size_t>(bytes, 16), h->stream) != cudaSuccess) return nullptr;
             h->allocs.push_back(p);
             return p;
         };
@@ -570,7 +590,6 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     CKL(dalloc(h, &G.succ, N1));
     CKL(dalloc(h, &G.jl, N1));
     CKL(dalloc(h, &G.top, N1));
-    CKL(dalloc(h, &G.val, N1 * dp));
     CKL(dalloc(h, &G.cpx, N1 * 8));
     CKL(dalloc(h, &G.hard, N1));
     CKL(dalloc(h, &G.swl, N1));
@@ -582,7 +601,6 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     for (int i = 0; i < L.d; i++) odd[i] = (uint8_t)(L.D[i] & 1);
     CKL(cudaMemcpyAsync(oddp, odd.data(), odd.size(), cudaMemcpyHostToDevice, s));
     if (L.d) CKL(cudaMemcpyAsync(h->d_D, L.D.data(), sizeof(int32_t) * L.d, cudaMemcpyHostToDevice, s));
-    CKL(cudaMemsetAsync(G.val, 0, sizeof(int32_t) * N1 * dp, s));   // sink row = 0
     CKL(cudaMemsetAsync(G.top, 0, N1, s));
     CKL(cudaMemsetAsync(G.cpx, 0, sizeof(uint32_t) * N1 * 8, s));   // sink prefix = zero row
     // incremental-valuation state (§V-inc)
