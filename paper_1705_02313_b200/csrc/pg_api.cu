@@ -53,6 +53,7 @@ struct pg_game_s {
     uint32_t epoch = 0;
     bool trace = false;               // PGSI_TRACE=1 (debug)
     bool c_valid = false;             // C covers every change since the last All_Even
+    int64_t inc_s_div = 64;           // incremental step when |S| * inc_s_div <= n'
     uint32_t cepoch = 0;
 };
 
@@ -269,7 +270,7 @@ void note_valuation(pg_game h, bool full_rows, bool inc) {
 // Incremental valuation pays off when the last switch step changed few choices.
 bool use_inc(pg_game h) {
     return h->have_state && h->G.dp <= 32 && h->last_nsw > 0 && !(h->flags & PG_NO_INCREMENTAL) &&
-           !(h->flags & PG_CHECK_INVARIANTS) && h->last_nsw * 64 <= h->G.n_int;
+           !(h->flags & PG_CHECK_INVARIANTS) && h->last_nsw * h->inc_s_div <= h->G.n_int;
 }
 
 // valuation + one switch step; redone in full if the splitter buffers overflowed
@@ -616,8 +617,10 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     G.epoch = 0;
     G.cepoch = 1;
     h->cepoch = 1;
-    G.inc_max_levels = 48;
-    G.inc_max_dirty = std::max<int64_t>(4096, L.n_int / 8);
+    // incremental-step thresholds (tuning knobs; results never depend on them)
+    G.inc_max_levels = getenv("PGSI_INC_MAX_LEVELS") ? atoi(getenv("PGSI_INC_MAX_LEVELS")) : 48;
+    G.inc_max_dirty = std::max<int64_t>(4096, L.n_int / (getenv("PGSI_INC_DIRTY_DIV") ? atoi(getenv("PGSI_INC_DIRTY_DIV")) : 8));
+    h->inc_s_div = getenv("PGSI_INC_S_DIV") ? atoi(getenv("PGSI_INC_S_DIV")) : 64;
     CKL(cudaMemsetAsync(G.ctl, 0, sizeof(Ctl), s));
     // splitter buffers: grown on demand (overflow protocol in valuate_and_switch)
     {

@@ -804,26 +804,42 @@ __device__ __forceinline__ int cmp_cpx(const uint32_t (&a)[8], const uint32_t (&
 }
 
 // Full lexicographic compare of val(a), val(b) (both finite, or the sink) when the
-// prefixes tie: both rows are rebuilt chunk by chunk, highest chunk first, by
-// walking the plays to the sink (full rows are not kept in HBM; the splitter
-// rows may be stale after incremental valuations). Rare (pg_stats.full_compares).
+// prefixes tie. The plays of a and b end in a common suffix (at the latest the
+// sink) that adds the same counts to both rows, and ⊑ is invariant under adding
+// the same vector (maxdiff and its sign are unchanged), so only the prefixes
+// before the plays merge are counted: walk the deeper play up to equal depth
+// (depths from jl), then both in lockstep until they meet. Rare
+// (pg_stats.full_compares); full rows are never stored.
 __device__ __noinline__ int cmp_full(const DevGame &g, int32_t a, int32_t b) {
     const int32_t N = (int32_t)g.n_int;
     const int nchunk = g.dp > 32 ? g.dp / 32 : 1;
+    const uint32_t da0 = a == N ? 0u : (uint32_t)(__ldcg(g.jl + a) >> 32);
+    const uint32_t db0 = b == N ? 0u : (uint32_t)(__ldcg(g.jl + b) >> 32);
     for (int c = nchunk - 1; c >= 0; c--) {
         int32_t ca[32], cb[32];
         for (int k = 0; k < 32; k++) { ca[k] = 0; cb[k] = 0; }
-        int64_t guard = 0;
-        for (int32_t x = a; x != N && guard <= N; guard++) {
+        int32_t x = a, y = b;
+        uint32_t dx = da0, dy = db0;
+        while (dx > dy) {
             const uint32_t p = (uint32_t)__ldg(g.pidx + x) - 32u * c;
             if (p < 32u) ca[p]++;
             x = __ldg(g.succ + x);
+            dx--;
         }
-        guard = 0;
-        for (int32_t x = b; x != N && guard <= N; guard++) {
-            const uint32_t p = (uint32_t)__ldg(g.pidx + x) - 32u * c;
+        while (dy > dx) {
+            const uint32_t p = (uint32_t)__ldg(g.pidx + y) - 32u * c;
             if (p < 32u) cb[p]++;
+            y = __ldg(g.succ + y);
+            dy--;
+        }
+        while (x != y && dx > 0) {
+            const uint32_t p = (uint32_t)__ldg(g.pidx + x) - 32u * c;
+            const uint32_t q = (uint32_t)__ldg(g.pidx + y) - 32u * c;
+            if (p < 32u) ca[p]++;
+            if (q < 32u) cb[q]++;
             x = __ldg(g.succ + x);
+            y = __ldg(g.succ + y);
+            dx--;
         }
         for (int col = min(32 * c + 31, g.dp - 1); col >= 32 * c; col--) {
             int32_t ka = ca[col - 32 * c], kb = cb[col - 32 * c];
