@@ -40,6 +40,12 @@ WORKLOADS = {
                  desc="random parity game n=1M, d=16, out-degree 2-5 (BASELINE configs[1])"),
     "cfg3": dict(n=10_000_000, d=32, lo=2, hi=5, ref_iters=1, cpu_iters=3,
                  desc="random parity game n=10M, d=32, out-degree 2-5 (BASELINE configs[2])"),
+    "cfg5": dict(n=100_000_000, d=32, lo=2, hi=5, ref_iters=1, cpu_iters=1,
+                 desc="random parity game n=100M, d=32, out-degree 2-5 (BASELINE configs[4], one GPU)"),
+    "ladder": dict(family="ladder", n=4_000_000, ref_iters=1, cpu_iters=2,
+                   desc="ladder family Lad(4M), d<=3 (BASELINE configs[3])"),
+    "hanoi": dict(family="hanoi", k=13, ref_iters=2, cpu_iters=4,
+                  desc="Towers-of-Hanoi family k=13 (3.19M vertices, d=3; BASELINE configs[3])"),
 }
 THROTTLE_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
                  0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
@@ -106,6 +112,11 @@ class ClockSampler:
 
 def make_game(wl, seed):
     import pg_inputs as gi
+    fam = wl.get("family")
+    if fam == "ladder":
+        return gi.ladder(wl["n"], seed)
+    if fam == "hanoi":
+        return gi.hanoi(wl["k"])
     return gi.random_game(wl["n"], wl["d"], wl["lo"], wl["hi"], seed)
 
 
@@ -148,7 +159,7 @@ def run_reference(args, wl, rank):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot_s / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
-        "data": "synthetic", "config": {"workload": wl["desc"], "n": wl["n"], "d": wl["d"],
+        "data": "synthetic", "config": {"workload": wl["desc"], "n": game.n, "d": wl.get("d"),
                                         "seed": args.seed, "parallelism": "cpu-1thread"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -181,16 +192,14 @@ def main():
     import numpy as np
     import torch
     torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_1705_02313_b200 import Game, _build
+    from paper_1705_02313_b200 import dist as pgdist
+    dist = pgdist.init("nccl", device=torch.device("cuda", local))   # None on one process
     _build.build()
 
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
-    game = make_game(wl, args.seed + rank)   # weak scaling: an independent game per rank
+    game = make_game(wl, pgdist.game_seed(args.seed, rank))   # weak scaling: an independent game per rank
     G = Game.from_game(game, device=local, stream=stream.cuda_stream, device_ptrs=True,
                        phase_timing=True)
     n = game.n
@@ -198,8 +207,7 @@ def main():
            torch.empty(n, dtype=torch.int32, device=dev), None)
 
     def barrier():
-        if dist is not None:
-            dist.barrier()
+        pgdist.barrier(dist)
 
     for _ in range(args.warmup):
         G.solve(out=out)
@@ -225,15 +233,7 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize(dev)
     barrier()
-    ms = e0.elapsed_time(e1)
-    units = float(n) * acc["inner_iters"]
-    if dist is not None:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-        u = torch.tensor([units], device=dev, dtype=torch.float64)
-        dist.all_reduce(u, op=dist.ReduceOp.SUM)
-        units = float(u.item())
+    ms, units = pgdist.reduce_time_and_units(dist, e0.elapsed_time(e1), float(n) * acc["inner_iters"], dev)
     value = units / (ms / 1000.0)
     inner = int(acc["inner_iters"] / args.steps)
     outer = int(acc["outer_passes"] / args.steps)
@@ -273,14 +273,7 @@ def main():
             s_units += float(n) * rs.stats["inner_iters"]
         e1.record(stream)
         torch.cuda.synchronize(dev)
-        sms = e0.elapsed_time(e1)
-        if dist is not None:
-            t = torch.tensor([sms], device=dev, dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            sms = float(t.item())
-            u = torch.tensor([s_units], device=dev, dtype=torch.float64)
-            dist.all_reduce(u, op=dist.ReduceOp.SUM)
-            s_units = float(u.item())
+        sms, s_units = pgdist.reduce_time_and_units(dist, e0.elapsed_time(e1), s_units, dev)
         scratch = {"value": s_units / (sms / 1000.0), "ms_per_step": sms / args.steps,
                    "note": "PG_NO_INCREMENTAL: every valuation recomputed for all vertices"}
         Gs.free()
@@ -313,13 +306,7 @@ def main():
         torch.cuda.synchronize(dev)
         ems = e0.elapsed_time(e1)
         wall_ms = 1000 * (time.perf_counter() - t0)
-        ems = max(ems, wall_ms)
-        if dist is not None:
-            t = torch.tensor([ems, e_units], device=dev, dtype=torch.float64)
-            tt = t.clone()
-            dist.all_reduce(t[0:1], op=dist.ReduceOp.MAX)
-            dist.all_reduce(tt[1:2], op=dist.ReduceOp.SUM)
-            ems, e_units = float(t[0].item()), float(tt[1].item())
+        ems, e_units = pgdist.reduce_time_and_units(dist, max(ems, wall_ms), e_units, dev)
         e2e = {"value": e_units / (ems / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": ems / e2e_steps, "steps": e2e_steps,
                "includes": "pg_load (H2D of the raw CSR, then validate / canonicalise / preprocess / reorder on the GPU) + pg_solve + D2H of winner, sigma, tau"}
@@ -340,7 +327,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-            "config": {"workload": wl["desc"], "n": n, "d": G.d, "out_degree": f"{wl['lo']}-{wl['hi']}",
+            "config": {"workload": wl["desc"], "n": n, "d": G.d, "out_degree": f"{wl.get('lo', '-')}-{wl.get('hi', '-')}",
                        "seed": args.seed, "n_internal": G.n_internal, "m": int(game.m),
                        "inner_iters": inner, "outer_passes": outer, "solve_ms": ms / args.steps,
                        "full_compares_per_solve": int(acc["full_compares"] / args.steps),
