@@ -993,6 +993,60 @@ __device__ __forceinline__ void warp_append(bool app, int32_t val, int32_t *list
     if (app) list[b + __popc(m & ((1u << lane) - 1u))] = val;
 }
 
+// Warp-cooperative append of up to 8 marked entries per lane: one warp scan and
+// one atomicAdd per warp (all lanes must call it).
+__device__ __forceinline__ void warp_append8(const int32_t (&u)[8], const bool (&ok)[8], int32_t *list,
+                                             unsigned long long *cnt) {
+    const int lane = threadIdx.x & 31;
+    int c = 0;
+#pragma unroll
+    for (int j = 0; j < 8; j++) c += ok[j];
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += t;
+    }
+    const int total = __shfl_sync(FULL, incl, 31);
+    if (total == 0) return;
+    unsigned long long base = 0;
+    if (lane == 31) base = atomicAdd(cnt, (unsigned long long)total);
+    base = __shfl_sync(FULL, base, 31);
+    unsigned long long pos = base + (unsigned long long)(incl - c);
+#pragma unroll
+    for (int j = 0; j < 8; j++)
+        if (ok[j]) list[pos++] = u[j];
+}
+
+// Expand the reverse edges [rb, re) of item f (-1 = none) 8 at a time with the
+// loads and atomics of a batch issued together. MODE 0: functional children of f
+// (succ(u) == f) newly marked in mark (D closure); MODE 1: Odd predecessors
+// (u >= lo_owner) newly marked (E); MODE 2: Even predecessors (u < n_even).
+template <int MODE>
+__device__ __forceinline__ void expand_rev(const DevGame &g, int32_t f, uint32_t rb, uint32_t re, uint32_t *mark,
+                                           uint32_t ep, int32_t *out, unsigned long long *cnt) {
+    const int maxd = (int)__reduce_max_sync(FULL, re - rb);
+    for (int k0 = 0; k0 < maxd; k0 += 8) {
+        int32_t u[8];
+        bool ok[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) u[j] = (rb + k0 + j < re) ? __ldg(g.rcol + rb + k0 + j) : -1;
+        if constexpr (MODE == 0) {
+#pragma unroll
+            for (int j = 0; j < 8; j++) ok[j] = u[j] >= 0 && __ldcg(g.succ + u[j]) == f;
+        } else if constexpr (MODE == 1) {
+#pragma unroll
+            for (int j = 0; j < 8; j++) ok[j] = u[j] >= 0 && u[j] >= g.n_even;
+        } else {
+#pragma unroll
+            for (int j = 0; j < 8; j++) ok[j] = u[j] >= 0 && u[j] < g.n_even;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; j++) ok[j] = ok[j] && atomicExch(mark + u[j], ep) != ep;
+        warp_append8(u, ok, out, cnt);
+    }
+}
+
 __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
     __shared__ uint8_t hsm[kThreads][36];
     __shared__ uint32_t osm[kThreads][9];
@@ -1029,16 +1083,7 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
                 rb = __ldg(g.rrp + f);
                 re = __ldg(g.rrp + f + 1);
             }
-            const int maxd = (int)__reduce_max_sync(FULL, re - rb);
-            for (int k = 0; k < maxd; k++) {
-                bool add = false;
-                int32_t u = -1;
-                if (rb + k < re) {
-                    u = __ldg(g.rcol + rb + k);
-                    add = __ldcg(g.succ + u) == f && atomicExch(g.dmark + u, ep) != ep;
-                }
-                warp_append(add, u, out, cnt);
-            }
+            expand_rev<0>(g, f, rb, re, g.dmark, ep, out, cnt);
         }
         gbar(ctl);
         const int64_t added = (int64_t)*(volatile unsigned long long *)cnt;
@@ -1143,16 +1188,7 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
             rb = __ldg(g.rrp + f);
             re = __ldg(g.rrp + f + 1);
         }
-        const int maxd = (int)__reduce_max_sync(FULL, re - rb);
-        for (int k = 0; k < maxd; k++) {
-            bool add = false;
-            int32_t p = -1;
-            if (rb + k < re) {
-                p = __ldg(g.rcol + rb + k);
-                add = p >= g.n_even && atomicExch(g.emark + p, ep) != ep;
-            }
-            warp_append(add, p, g.El, &ctl->nE);
-        }
+        expand_rev<1>(g, -1, rb, re, g.emark, ep, g.El, &ctl->nE);
     }
     gbar(ctl);
     const int64_t ne = (int64_t)*(volatile unsigned long long *)&ctl->nE;
@@ -1216,16 +1252,7 @@ __global__ void __launch_bounds__(kThreads) k_ebuild_even(DevGame g) {
             rb = __ldg(g.rrp + f);
             re = __ldg(g.rrp + f + 1);
         }
-        const int maxd = (int)__reduce_max_sync(FULL, re - rb);
-        for (int k = 0; k < maxd; k++) {
-            bool add = false;
-            int32_t p = -1;
-            if (rb + k < re) {
-                p = __ldg(g.rcol + rb + k);
-                add = p < g.n_even && atomicExch(g.emark + p, ep) != ep;
-            }
-            warp_append(add, p, g.El, &g.ctl->nE);
-        }
+        expand_rev<2>(g, -1, rb, re, g.emark, ep, g.El, &g.ctl->nE);
     }
 }
 
