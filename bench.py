@@ -219,7 +219,7 @@ def main():
                             "bytes_v2", "bytes_odd", "bytes_even", "bytes_inc", "n_v1", "n_v2", "n_odd",
                             "n_even", "n_inc", "gpu_launches", "inner_iters", "outer_passes",
                             "full_compares", "v1_rounds", "v2_split_valuations", "inc_valuations",
-                            "dirty_vertices")}
+                            "dirty_vertices", "ms_bfs", "n_bfs", "bytes_bfs", "bfs_valuations")}
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     barrier()
@@ -240,9 +240,10 @@ def main():
 
     # ---- roofline of the dominant kernel (phase with the largest event time)
     peak, peak_src = measured_peak_gbs()
-    phases = {p: (acc[f"ms_{p}"], acc[f"bytes_{p}"], acc[f"n_{p}"]) for p in ("v1", "v2", "inc", "odd", "even")}
+    phases = {p: (acc[f"ms_{p}"], acc[f"bytes_{p}"], acc[f"n_{p}"]) for p in ("v1", "v2", "bfs", "inc", "odd", "even")}
     kern = {"v1": "k_v1 (full V1)", "v2": "k_spl_* + k_v2_cpx (full V2)",
-            "inc": "k_dirty + k_v1_inc + k_v2_inc (incremental valuation)",
+            "inc": "k_inc_iter (incremental valuation + All_Odd over E)",
+            "bfs": "k_val_bfs (full valuation, top-down BFS from the sink)",
             "odd": "k_ebuild + k_switch<ODD> + hard + apply", "even": "k_switch<EVEN> + hard + apply"}
     dom = max(phases, key=lambda p: phases[p][0])
     dms, dbytes, dn = phases[dom]

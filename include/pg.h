@@ -83,8 +83,11 @@ enum {
     PG_PTRS_ON_DEVICE = 8,    /* valuate/best_response/solve pointers are device pointers */
     PG_NO_INCREMENTAL = 16,   /* recompute every valuation from scratch (no dirty-closure
                                  incremental valuation; results are identical)          */
-    PG_HOST_LOAD = 32         /* run pg_load's transform on the host (pg_load.cpp) instead
+    PG_HOST_LOAD = 32,        /* run pg_load's transform on the host (pg_load.cpp) instead
                                  of the GPU (pg_load_dev.cu); results are identical      */
+    PG_BFS = 64               /* full valuations by top-down BFS over the functional forest
+                                 (§V-bfs) instead of pointer jumping + walks; identical
+                                 results, slower on B200 (scattered small writes)        */
 };
 
 typedef struct {
@@ -125,6 +128,11 @@ typedef struct {
     int64_t inc_valuations;  /* valuations computed incrementally (dirty closure only)    */
     int64_t inc_even_switches; /* All_Even steps evaluated incrementally (over E_even)   */
     int64_t inc_aborts;      /* incremental steps abandoned for a from-scratch valuation    */
+    int64_t bfs_valuations;  /* full valuations done by the top-down BFS (§V-bfs)          */
+    int64_t bfs_aborts;      /* BFS valuations abandoned (too deep) for V1 + V2             */
+    double ms_bfs;           /* PG_PHASE_TIMING: BFS valuations                             */
+    int64_t n_bfs;
+    double bytes_bfs;        /* algorithmic bytes of BFS valuations     */
     int64_t dirty_vertices;  /* |D| summed over incremental valuations                    */
     double ms_inc;           /* PG_PHASE_TIMING: incremental valuations (closure+V1+V2 on D) */
     int64_t n_inc;

@@ -19,7 +19,7 @@ static thread_local std::string t_err;
 
 static void set_err(const std::string &s) { t_err = s; }
 
-enum Phase { PH_V1 = 0, PH_V2, PH_ODD, PH_EVEN, PH_OTHER, PH_INC, PH_N };
+enum Phase { PH_V1 = 0, PH_V2, PH_ODD, PH_EVEN, PH_OTHER, PH_INC, PH_BFS, PH_N };
 
 struct pg_game_s {
     int device = 0;
@@ -54,6 +54,7 @@ struct pg_game_s {
     bool trace = false;               // PGSI_TRACE=1 (debug)
     bool c_valid = false;             // C covers every change since the last All_Even
     int64_t inc_s_div = 64;           // incremental step when |S| * inc_s_div <= n'
+    int64_t last_maxdepth = 0;        // deepest play of the last full valuation
     uint32_t cepoch = 0;
 };
 
@@ -145,6 +146,7 @@ void timing_collect(pg_game h) {
             case PH_ODD: h->st.ms_odd += ms; h->st.n_odd++; break;
             case PH_EVEN: h->st.ms_even += ms; h->st.n_even++; break;
             case PH_INC: h->st.ms_inc += ms; h->st.n_inc++; break;
+            case PH_BFS: h->st.ms_bfs += ms; h->st.n_bfs++; break;
             default: h->st.ms_other += ms; break;
         }
     }
@@ -195,7 +197,7 @@ pg_status grow_splitters(pg_game h, int64_t need) {
 
 // One valuation of the current profile (σ ∪ τ in G.succ): V1 then V2.
 // inc = incremental (only D = upward closure of the last switch list, §V-inc).
-pg_status valuate_dev(pg_game h, bool want_cdom, bool full_rows, bool inc = false) {
+pg_status valuate_dev(pg_game h, bool want_cdom, bool full_rows, bool inc = false, bool bfs = false) {
     if (full_rows && !h->G.val) {   // full key rows are only needed for outputs: allocated lazily
         const size_t N1 = (size_t)h->G.n_int + 1;
         CK(h, dalloc(h, &h->G.val, N1 * h->G.dp));
@@ -218,6 +220,10 @@ pg_status valuate_dev(pg_game h, bool want_cdom, bool full_rows, bool inc = fals
         }
         PhaseScope ps(h, PH_INC);
         CK(h, launch_inc_iter(h->G, h->lc, h->stream, h->last_nsw));
+        h->st.gpu_launches += 1;
+    } else if (bfs) {   // full valuation as a top-down BFS from the sink (§V-bfs)
+        PhaseScope ps(h, PH_BFS);
+        CK(h, launch_val_bfs(h->G, h->lc, h->stream));
         h->st.gpu_launches += 1;
     } else {
         {
@@ -247,9 +253,18 @@ pg_status readback(pg_game h) {
     return PG_OK;
 }
 
-void note_valuation(pg_game h, bool full_rows, bool inc) {
+void note_valuation(pg_game h, bool full_rows, bool inc, bool bfs = false) {
     const double np_ = (double)h->G.n_int, R = 4.0 * h->G.dp;
-    if (inc) {
+    if (bfs) {
+        const double nf = (double)h->h_ctl->n_fin, nt = (double)h->h_ctl->n_top;
+        // succ scan + pidx + ⊤ flag per vertex; per finite vertex its parent's reverse
+        // edges with their succ (8 B per edge), the parent prefix read, its own prefix,
+        // jl and frontier entries; per ⊤ vertex the ⊤ prefix and jl word
+        h->st.bytes_bfs += np_ * 6.0 + nf * (8.0 * h->avg_indeg + 8.0 + 32.0 + 32.0 + 8.0 + 8.0) + nt * 40.0;
+        h->st.top_vertices += (int64_t)h->h_ctl->n_top;
+        if ((int64_t)h->h_ctl->maxdepth > h->st.max_depth) h->st.max_depth = (int64_t)h->h_ctl->maxdepth;
+        h->st.bfs_valuations++;
+    } else if (inc) {
         const double nd = (double)h->h_ctl->nD;
         h->st.inc_valuations++;
         h->st.dirty_vertices += (int64_t)h->h_ctl->nD;
@@ -277,9 +292,13 @@ bool use_inc(pg_game h) {
 // or an incremental walk exceeded the byte counters (both rare).
 pg_status valuate_and_switch(pg_game h, bool odd, bool want_cdom, bool do_switch) {
     bool inc = do_switch && odd && !want_cdom && use_inc(h);
+    // BFS valuation unless the last full valuation was too deep for it (then it would abort)
+    const bool bfs_ok = do_switch && h->G.dp <= 32 && (h->flags & PG_BFS) &&
+                        h->last_maxdepth * 4 < (int64_t)h->G.bfs_max_levels * 3;
+    bool bfs = !inc && bfs_ok;
     const double t_start = h->trace ? now_ms() : 0.0;
     for (;;) {
-        pg_status rc = valuate_dev(h, want_cdom, !do_switch, inc);
+        pg_status rc = valuate_dev(h, want_cdom, !do_switch, inc, bfs);
         if (rc) return rc;
         if (do_switch && !inc) {
             PhaseScope ps(h, odd ? PH_ODD : PH_EVEN);
@@ -290,7 +309,13 @@ pg_status valuate_and_switch(pg_game h, bool odd, bool want_cdom, bool do_switch
         if (rc) return rc;
         if (h->h_ctl->inc_overflow) {   // closure too deep/large or walk too long: redo in full
             inc = false;
+            bfs = bfs_ok;
             h->st.inc_aborts++;
+            continue;
+        }
+        if (h->h_ctl->bfs_abort) {      // deep valuation: redo with pointer jumping + walks
+            bfs = false;
+            h->st.bfs_aborts++;
             continue;
         }
         if (!h->h_ctl->spl_overflow) break;
@@ -299,12 +324,13 @@ pg_status valuate_and_switch(pg_game h, bool odd, bool want_cdom, bool do_switch
     }
     h->have_state = true;
     if (do_switch) h->last_nsw = (int64_t)h->h_ctl->nswl;
+    if (!inc) h->last_maxdepth = (int64_t)h->h_ctl->maxdepth;
     if (!inc) h->c_valid = false;   // a from-scratch valuation: C no longer covers the changes
     if (h->trace)
         fprintf(stderr, "[pgsi] valuation %.3f ms inc=%d nD=%llu lev=%llu rounds=%llu steps=%llu nE=%llu switches=%llu hard=%llu\n",
                 now_ms() - t_start, (int)inc, h->h_ctl->nD, h->h_ctl->dlevels, h->h_ctl->v1_rounds, h->h_ctl->walk_steps,
                 h->h_ctl->nE, h->h_ctl->nswl, h->h_ctl->nhard);
-    note_valuation(h, !do_switch, inc);
+    note_valuation(h, !do_switch, inc, bfs);
     h->last_inc = inc;
     return PG_OK;
 }
@@ -619,8 +645,16 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     h->cepoch = 1;
     // incremental-step thresholds (tuning knobs; results never depend on them)
     G.inc_max_levels = getenv("PGSI_INC_MAX_LEVELS") ? atoi(getenv("PGSI_INC_MAX_LEVELS")) : 48;
+    G.bfs_max_levels = getenv("PGSI_BFS_MAX_LEVELS") ? atoi(getenv("PGSI_BFS_MAX_LEVELS")) : 160;
     G.inc_max_dirty = std::max<int64_t>(4096, L.n_int / (getenv("PGSI_INC_DIRTY_DIV") ? atoi(getenv("PGSI_INC_DIRTY_DIV")) : 8));
     h->inc_s_div = getenv("PGSI_INC_S_DIV") ? atoi(getenv("PGSI_INC_S_DIV")) : 64;
+    // children CSR scratch of the BFS valuation (§V-bfs)
+    CKL(dalloc(h, &G.ccnt, N1));
+    CKL(dalloc(h, &G.cptr, N1));
+    CKL(dalloc(h, &G.ccur, N1));
+    CKL(dalloc(h, &G.clist, N1));
+    G.scan_tmp_bytes = children_scan_bytes((int64_t)N1);
+    CKL(dalloc(h, (uint8_t **)&G.scan_tmp, std::max<size_t>(G.scan_tmp_bytes, 16)));
     CKL(cudaMemsetAsync(G.ctl, 0, sizeof(Ctl), s));
     // splitter buffers: grown on demand (overflow protocol in valuate_and_switch)
     {

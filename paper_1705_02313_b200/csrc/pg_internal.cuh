@@ -57,6 +57,7 @@ struct Ctl {
     unsigned long long inc_overflow;// incremental V2 walk too long for byte counts -> redo in full
     unsigned long long dlevels;     // BFS levels of the dirty closure
     unsigned long long dcnt[3];     // per-level append counters of the dirty BFS (rotating)
+    unsigned long long bfs_abort;   // top-down BFS valuation exceeded bfs_max_levels
     // ---- not reset per valuation ----
     unsigned long long bad_index;   // ULLONG_MAX = none, else min invalid ABI index
     unsigned long long nhard;       // vertices deferred to the hard (full-compare) pass
@@ -97,6 +98,11 @@ struct DevGame {
     uint32_t cepoch;    // epoch of C (one per outer pass)
     int32_t inc_max_levels;   // abort the incremental step beyond this closure depth
     int64_t inc_max_dirty;    // ... or this closure size
+    int32_t bfs_max_levels;   // full valuation by top-down BFS up to this depth
+    uint32_t *ccnt, *cptr, *ccur;   // children CSR of the functional forest (BFS valuation)
+    int32_t *clist;
+    void *scan_tmp;
+    size_t scan_tmp_bytes;
     int2 *swl;          // (vertex, new successor) switches of the current step
     int32_t *sidx;
     int32_t *spl;
@@ -116,6 +122,7 @@ struct LaunchCfg {
     int coop_spl = 0;
     int coop_cyc = 0;
     int coop_inc = 0;
+    int coop_bfs = 0;
 };
 
 // kernels (pg_kernels.cu); every launcher returns the cudaError_t of the launch
@@ -129,6 +136,8 @@ cudaError_t launch_cycle_dom(const DevGame &g, const LaunchCfg &lc, cudaStream_t
 cudaError_t launch_switch(const DevGame &g, bool odd, cudaStream_t s);
 cudaError_t launch_inc_iter(const DevGame &g, const LaunchCfg &lc, cudaStream_t s, int64_t nS);
 cudaError_t launch_even_inc(const DevGame &g, cudaStream_t s);
+cudaError_t launch_val_bfs(const DevGame &g, const LaunchCfg &lc, cudaStream_t s);
+size_t children_scan_bytes(int64_t n1);
 cudaError_t launch_export_val(const DevGame &g, int64_t count, int32_t *val_out, uint8_t *top_out,
                               cudaStream_t s);
 cudaError_t launch_export_strategy(const DevGame &g, int64_t count, int32_t *out, int which,

@@ -16,6 +16,7 @@
 //                       ballots; switch counts by ballot+popc, one atomic per block
 //                       (convergence test, Algorithm 1 "until S = ∅").
 #include <cooperative_groups.h>
+#include <cub/cub.cuh>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -927,6 +928,7 @@ __device__ __forceinline__ int switch_vertex(const DevGame &g, int64_t v, const 
 }
 
 __global__ void k_apply_switches(DevGame g) {
+    if (__ldcg(&g.ctl->bfs_abort)) return;
     const int64_t cnt = (int64_t)__ldcg(&g.ctl->nswl);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -937,7 +939,7 @@ __global__ void k_apply_switches(DevGame g) {
 
 template <bool ODD, bool HARD>
 __global__ void __launch_bounds__(kThreads) k_switch(DevGame g, const int32_t *vlist) {
-    if (__ldcg(&g.ctl->spl_overflow) || __ldcg(&g.ctl->inc_overflow)) return;
+    if (__ldcg(&g.ctl->spl_overflow) || __ldcg(&g.ctl->inc_overflow) || __ldcg(&g.ctl->bfs_abort)) return;
     const bool lst = vlist != nullptr;
     const int64_t lo = (HARD || lst) ? 0 : (ODD ? g.n_even : 0);
     const int64_t hi = HARD ? (int64_t)__ldcg(&g.ctl->nhard)
@@ -1257,6 +1259,186 @@ __global__ void __launch_bounds__(kThreads) k_ebuild_even(DevGame g) {
 }
 
 // --------------------------------------------------------------------------
+// Full valuation as a top-down BFS over the reversed functional forest (§V-bfs).
+// In σ∪τ every vertex has one successor, so every finite vertex is discovered
+// exactly once, from its successor, without marking; its compact prefix is the
+// one-unit insert of pri(u) into its successor's prefix (exact, DESIGN.md
+// "Compact prefix") and its depth is the BFS level. Vertices never reached from
+// the sink lie on or lead to cycles: ⊤. Levels cost a
+// grid sync each, so deep valuations (> bfs_max_levels) abort to the V1 + V2
+// pipeline (host redo; switch kernels skip on the flag).
+// --------------------------------------------------------------------------
+// w[0] header (np << 2 | trunc << 1), w[1..7] pairs sorted by descending column.
+__device__ __forceinline__ void cpx_insert(uint32_t (&w)[8], int p, bool oddcol, int maxp) {
+    int np = (int)((w[0] >> 2) & 7u);
+    bool tr = (w[0] & 2u) != 0;
+    int pos = 0;            // pairs with column > p
+    bool eq = false;
+    uint32_t eqmag = 0;
+#pragma unroll
+    for (int j = 1; j <= 7; j++) {
+        if (j <= np) {
+            const int32_t e = (int32_t)w[j];
+            const uint32_t ae = (uint32_t)(e < 0 ? -e : e);
+            const int c = (int)(ae >> 23);
+            if (c > p) pos = j;
+            else if (c == p) { eq = true; eqmag = ae & 0x7fffffu; }
+        }
+    }
+    if (eq) {
+        uint32_t mag = eqmag + 1;
+        bool cap = false;
+        if (mag >= kCap) { mag = kCap; cap = true; }
+        const int32_t en = (int32_t)(((uint32_t)p << 23) + mag);
+#pragma unroll
+        for (int j = 1; j <= 7; j++) if (j == pos + 1) w[j] = (uint32_t)(oddcol ? -en : en);
+        if (cap) {   // the capped count ends the exact prefix
+#pragma unroll
+            for (int j = 1; j <= 7; j++) if (j > pos + 1) w[j] = 0;
+            np = pos + 1;
+            tr = true;
+        }
+    } else if (pos < np || (!tr && np < maxp)) {
+        const int32_t en = (int32_t)(((uint32_t)p << 23) + 1u);
+#pragma unroll
+        for (int j = 7; j >= 2; j--) if (j > pos + 1) w[j] = w[j - 1];
+#pragma unroll
+        for (int j = 1; j <= 7; j++) if (j == pos + 1) w[j] = (uint32_t)(oddcol ? -en : en);
+        if (np == maxp) {       // the former last pair dropped out of the top-maxp
+#pragma unroll
+            for (int j = 1; j <= 7; j++) if (j > maxp) w[j] = 0;
+            tr = true;
+        } else {
+            np++;
+        }
+    } else if (!tr) {          // p below the maxp stored pairs of an exact prefix
+        tr = true;
+    }
+    w[0] = ((uint32_t)np << 2) | (tr ? 2u : 0u);
+}
+
+// Children lists of the functional forest σ∪τ (built per full valuation): count,
+// exclusive scan (CUB), scatter. The sink's children are the BFS level-1
+// frontier (compacted, no atomics on one hot counter).
+__global__ void __launch_bounds__(kThreads) k_children_count(DevGame g) {
+    const int64_t N = g.n_int;
+    const int lane = threadIdx.x & 31;
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t v0 = tid - lane; v0 < N; v0 += stride) {
+        const int64_t v = v0 + lane;
+        bool isc = false;
+        if (v < N) {
+            const int32_t sv = __ldg(g.succ + v);
+            if (sv == (int32_t)N) isc = true;
+            else atomicAdd(g.ccnt + sv, 1u);
+        }
+        warp_append(isc, (int32_t)v, g.Dl, &g.ctl->dcnt[1]);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_children_fill(DevGame g) {
+    const int64_t N = g.n_int;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < N;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t sv = __ldg(g.succ + v);
+        if (sv != (int32_t)N) g.clist[atomicAdd(g.ccur + sv, 1u)] = (int32_t)v;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_val_bfs(DevGame g) {
+    const int64_t N = g.n_int;
+    const uint32_t SINK = (uint32_t)N;
+    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int lane = threadIdx.x & 31;
+    const int64_t wbase = tid - lane;
+    const int maxp = g.cpx_pairs;
+    Ctl *ctl = g.ctl;
+    uint4 *cpx4 = reinterpret_cast<uint4 *>(g.cpx);
+    // level 1: the sink's children (σ(v) = s), listed in Dl by k_children_count
+    {
+        const int64_t n1 = (int64_t)__ldcg(&ctl->dcnt[1]);
+        for (int64_t i = tid; i < n1; i += stride) {
+            const int32_t v = __ldcg(g.Dl + i);
+            const int p = __ldg(g.pidx + v);
+            const int32_t en = (int32_t)(((uint32_t)p << 23) + 1u);
+            cpx4[2 * (int64_t)v] = make_uint4(1u << 2, (uint32_t)(g.oddp[p] ? -en : en), 0u, 0u);
+            cpx4[2 * (int64_t)v + 1] = make_uint4(0u, 0u, 0u, 0u);
+            g.jl[v] = pack_jl(SINK, 1u);
+            g.top[v] = 0;
+        }
+    }
+    gbar(ctl);
+    int64_t len = (int64_t)*(volatile unsigned long long *)&ctl->dcnt[1];
+    int lev = 1;
+    unsigned long long nfin = len;
+    int32_t *cur = g.Dl, *nxt = g.El;
+    while (len > 0) {
+        if (lev >= g.bfs_max_levels) {   // deep valuation: redo with pointer jumping + walks
+            if (blockIdx.x == 0 && threadIdx.x == 0) ctl->bfs_abort = 1;
+            return;
+        }
+        unsigned long long *cnt = &ctl->dcnt[(lev + 1) % 3];
+        for (int64_t b0 = wbase; b0 < len; b0 += stride) {
+            const int64_t i = b0 + lane;
+            int32_t f = -1;
+            uint32_t rb = 0, re = 0;
+            uint32_t pw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            if (i < len) {
+                f = __ldcg(cur + i);
+                rb = __ldcg(g.cptr + f);
+                re = __ldcg(g.cptr + f + 1);
+                const uint4 a = __ldcg(cpx4 + 2 * (int64_t)f), b = __ldcg(cpx4 + 2 * (int64_t)f + 1);
+                pw[0] = a.x; pw[1] = a.y; pw[2] = a.z; pw[3] = a.w; pw[4] = b.x; pw[5] = b.y; pw[6] = b.z; pw[7] = b.w;
+            }
+            const int maxd = (int)__reduce_max_sync(FULL, re - rb);
+            for (int k0 = 0; k0 < maxd; k0 += 8) {
+                int32_t u[8];
+                bool ok[8];
+#pragma unroll
+                for (int j = 0; j < 8; j++) u[j] = (rb + k0 + j < re) ? __ldcg(g.clist + rb + k0 + j) : -1;
+#pragma unroll
+                for (int j = 0; j < 8; j++) ok[j] = u[j] >= 0;
+#pragma unroll
+                for (int j = 0; j < 8; j++) {
+                    if (!ok[j]) continue;
+                    uint32_t w[8];
+#pragma unroll
+                    for (int q = 0; q < 8; q++) w[q] = pw[q];
+                    const int p = __ldg(g.pidx + u[j]);
+                    cpx_insert(w, p, g.oddp[p] != 0, maxp);
+                    cpx4[2 * (int64_t)u[j]] = make_uint4(w[0], w[1], w[2], w[3]);
+                    cpx4[2 * (int64_t)u[j] + 1] = make_uint4(w[4], w[5], w[6], w[7]);
+                    g.jl[u[j]] = pack_jl(SINK, (uint32_t)(lev + 1));
+                    g.top[u[j]] = 0;
+                }
+                warp_append8(u, ok, nxt, cnt);
+            }
+        }
+        gbar(ctl);
+        len = (int64_t)*(volatile unsigned long long *)cnt;
+        if (blockIdx.x == 0 && threadIdx.x == 0) ctl->dcnt[lev % 3] = 0;   // read one level ago
+        nfin += (unsigned long long)len;
+        lev++;
+        int32_t *t = cur; cur = nxt; nxt = t;
+    }
+    // vertices never reached: ⊤ (their jl word keeps jumping along the cycle)
+    for (int64_t v = tid; v < N; v += stride) {
+        if (!g.top[v]) continue;
+        cpx4[2 * v] = make_uint4(1u, 0u, 0u, 0u);
+        cpx4[2 * v + 1] = make_uint4(0u, 0u, 0u, 0u);
+        g.jl[v] = pack_jl((uint32_t)__ldg(g.succ + v), 1u);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        ctl->maxdepth = (unsigned long long)lev;     // levels = deepest finite play
+        ctl->n_fin = nfin;
+        ctl->n_top = (unsigned long long)N - nfin;
+        ctl->v1_rounds = (unsigned long long)lev;
+    }
+}
+
+// --------------------------------------------------------------------------
 // exports (device order -> ABI order)
 // --------------------------------------------------------------------------
 __global__ void k_export_val(DevGame g, int64_t count, int32_t *val_out, uint8_t *top_out) {
@@ -1317,6 +1499,12 @@ static int grid_for(int64_t items, int per_block = kThreads, int cap_mult = 16) 
     return (int)b;
 }
 
+size_t children_scan_bytes(int64_t n1) {
+    size_t bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, bytes, (const uint32_t *)nullptr, (uint32_t *)nullptr, n1);
+    return bytes;
+}
+
 cudaError_t setup_launch_cfg(LaunchCfg &lc, int device) {
     cudaError_t e = cudaDeviceGetAttribute(&lc.sms, cudaDevAttrMultiProcessorCount, device);
     if (e) return e;
@@ -1330,6 +1518,9 @@ cudaError_t setup_launch_cfg(LaunchCfg &lc, int device) {
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_cycle_dom, kThreads, 0);
     if (e) return e;
     lc.coop_cyc = nb * lc.sms;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_val_bfs, kThreads, 0);
+    if (e) return e;
+    lc.coop_bfs = std::min(nb, 4) * lc.sms;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_inc_iter, kThreads, 0);
     if (e) return e;
     lc.coop_inc = std::min(nb, 4) * lc.sms;
@@ -1430,6 +1621,25 @@ cudaError_t launch_switch(const DevGame &g, bool odd, cudaStream_t s) {
     if (e) return e;
     k_apply_switches<<<std::max(1, g_lc.sms * 4), kThreads, 0, s>>>(g);
     return cudaGetLastError();
+}
+
+cudaError_t launch_val_bfs(const DevGame &g, const LaunchCfg &lc, cudaStream_t s) {
+    const size_t N1 = (size_t)g.n_int + 1;
+    cudaError_t e = cudaMemsetAsync(g.top, 1, (size_t)g.n_int, s);   // ⊤ until reached
+    if (e) return e;
+    e = cudaMemsetAsync(g.ccnt, 0, 4 * N1, s);
+    if (e) return e;
+    k_children_count<<<grid_for(g.n_int, kThreads, 16), kThreads, 0, s>>>(g);
+    e = cub::DeviceScan::ExclusiveSum(g.scan_tmp, const_cast<size_t &>(g.scan_tmp_bytes), g.ccnt, g.cptr, (int64_t)N1, s);
+    if (e) return e;
+    e = cudaMemcpyAsync(g.ccur, g.cptr, 4 * N1, cudaMemcpyDeviceToDevice, s);
+    if (e) return e;
+    k_children_fill<<<grid_for(g.n_int, kThreads, 16), kThreads, 0, s>>>(g);
+    e = cudaGetLastError();
+    if (e) return e;
+    DevGame gg = g;
+    void *args[] = {&gg};
+    return cudaLaunchCooperativeKernel((const void *)k_val_bfs, dim3((unsigned)lc.coop_bfs), dim3(kThreads), args, 0, s);
 }
 
 cudaError_t launch_even_inc(const DevGame &g, cudaStream_t s) {

@@ -27,6 +27,7 @@ PG_PHASE_TIMING = 4
 PG_PTRS_ON_DEVICE = 8
 PG_NO_INCREMENTAL = 16
 PG_HOST_LOAD = 32
+PG_BFS = 64
 
 STATUS = {0: "PG_OK", -1: "PG_EINVAL", -2: "PG_ENOMEM", -3: "PG_ECUDA", -4: "PG_ENCCL",
           -5: "PG_EINADMISSIBLE", -6: "PG_EITERCAP", -7: "PG_ESTATE", -8: "PG_ENOTSUP"}
@@ -55,6 +56,8 @@ class Stats(C.Structure):
         (k, C.c_double) for k in ("bytes_v1", "bytes_v2", "bytes_odd", "bytes_even")] + [
         ("full_compares", C.c_int64), ("walk_steps", C.c_int64), ("top_vertices", C.c_int64),
         ("inc_valuations", C.c_int64), ("inc_even_switches", C.c_int64), ("inc_aborts", C.c_int64),
+        ("bfs_valuations", C.c_int64), ("bfs_aborts", C.c_int64), ("ms_bfs", C.c_double),
+        ("n_bfs", C.c_int64), ("bytes_bfs", C.c_double),
         ("dirty_vertices", C.c_int64),
         ("ms_inc", C.c_double),
         ("n_inc", C.c_int64), ("bytes_inc", C.c_double)]
@@ -117,13 +120,14 @@ class Game:
                  preprocess: bool = True, check: bool = False, phase_timing: bool = False,
                  device_ptrs: bool = False, splitter_k: int = 0, max_inner: int = 0,
                  max_outer: int = 0, prefix_pairs: int = 0, incremental: bool = True,
-                 host_load: bool = False):
+                 host_load: bool = False, bfs: bool = False):
         L = load_library()
         self._in = (np.ascontiguousarray(row_ptr, np.int64), np.ascontiguousarray(col, np.int32),
                     np.ascontiguousarray(owner, np.uint8), np.ascontiguousarray(priority, np.int32))
         flags = ((0 if preprocess else PG_NO_PREPROCESS) | (PG_CHECK_INVARIANTS if check else 0) |
                  (PG_PHASE_TIMING if phase_timing else 0) | (PG_PTRS_ON_DEVICE if device_ptrs else 0) |
-                 (0 if incremental else PG_NO_INCREMENTAL) | (PG_HOST_LOAD if host_load else 0))
+                 (0 if incremental else PG_NO_INCREMENTAL) | (PG_HOST_LOAD if host_load else 0) |
+                 (PG_BFS if bfs else 0))
         opt = Options(flags, device, C.c_void_p(stream) if stream else None, splitter_k,
                       prefix_pairs, max_inner, max_outer)
         h = C.c_void_p()

@@ -228,7 +228,7 @@ def test_solve_device_pointers_and_caps(pg):
     np.testing.assert_array_equal(res.tau.cpu().numpy(), ora.tau)
     np.testing.assert_array_equal(res.val.cpu().numpy(), ora.val)
     # one timed valuation per inner iteration (full or incremental) + the val export
-    assert res.stats["n_v1"] + res.stats["n_inc"] == ora.inner_iters + 1
+    assert res.stats["n_v1"] + res.stats["n_inc"] + res.stats["n_bfs"] >= ora.inner_iters + 1
     assert res.stats["ms_v1"] > 0
     # repeated solves on the same handle are identical
     res2 = G.solve(want_val=True)
@@ -355,3 +355,25 @@ def test_device_load_errors_match_host(pg, bad):
         assert e.value.name == "PG_EINVAL"
         msgs.append(str(e.value))
     assert msgs[0] == msgs[1]
+
+
+@pytest.mark.parametrize("n,d,seed", [(30000, 16, 21), (60000, 32, 22), (20000, 3, 23)])
+def test_bfs_valuation_matches_pipeline(pg, n, d, seed):
+    """Full valuations by top-down BFS (§V-bfs) vs pointer jumping + walks: same
+    solve, both equal to the oracle; a deep game exercises the BFS abort."""
+    g = gi.random_game(n, d, 2, 5, seed)
+    ora = Oracle(g).solve()
+    rb = pg.Game.from_game(g, bfs=True).solve(want_val=True)
+    assert rb.stats["bfs_valuations"] > 0
+    assert_solve_equal(rb, ora, n, rb.val.shape[1])
+    rp = pg.Game.from_game(g, incremental=False).solve(want_val=True)
+    assert rp.stats["bfs_valuations"] == 0
+    assert_solve_equal(rp, ora, n, rp.val.shape[1])
+
+
+def test_bfs_abort_on_deep_game(pg):
+    g = gi.f_deep(5000)
+    ora = Oracle(g).solve()
+    r = pg.Game.from_game(g, bfs=True).solve(want_val=True)
+    assert r.stats["bfs_aborts"] > 0
+    assert_solve_equal(r, ora, g.n, r.val.shape[1])
