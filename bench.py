@@ -46,6 +46,10 @@ WORKLOADS = {
                    desc="ladder family Lad(4M), d<=3 (BASELINE configs[3])"),
     "hanoi": dict(family="hanoi", k=13, ref_iters=2, cpu_iters=4,
                   desc="Towers-of-Hanoi family k=13 (3.19M vertices, d=3; BASELINE configs[3])"),
+    "elevator": dict(family="elevator", f=20, r=15, ref_iters=2, cpu_iters=4,
+                     desc="elevator family (f=20, r=15): 1.97M vertices, d=3 (BASELINE configs[3])"),
+    "stair": dict(family="stair", L=5000, ref_iters=200, cpu_iters=400,
+                  desc="F_stair(5000) long-iteration family: 5000 outer passes (BASELINE configs[4])"),
 }
 THROTTLE_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
                  0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
@@ -117,6 +121,10 @@ def make_game(wl, seed):
         return gi.ladder(wl["n"], seed)
     if fam == "hanoi":
         return gi.hanoi(wl["k"])
+    if fam == "elevator":
+        return gi.elevator(wl["f"], wl["r"], seed)
+    if fam == "stair":
+        return gi.f_stair(wl["L"])
     return gi.random_game(wl["n"], wl["d"], wl["lo"], wl["hi"], seed)
 
 

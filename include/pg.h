@@ -139,6 +139,9 @@ typedef struct {
     double bytes_inc;        /* algorithmic bytes of incremental valuations: per dirty vertex
                                 8·indeg (reverse edges + predecessor succ) + 62 B own state
                                 + 32 B exit prefix read               */
+    int64_t dist_exchanges;  /* switch-list exchanges with the other ranks (pg_dist_attach) */
+    int64_t dist_bytes;      /* device bytes this rank sent through the exchange            */
+    double ms_dist;          /* host wall time inside the exchange callback                 */
 } pg_stats;
 
 /* pg_load: validate, canonicalise and preprocess a game, copy it to the GPU.
@@ -215,6 +218,33 @@ pg_status pg_inspect(int64_t n, const int64_t *row_ptr, const int32_t *col,
                      int64_t *n_internal, int32_t *d, int64_t *dummies, int64_t *m_internal,
                      uint8_t *owner_int, int32_t *pidx_int, int64_t *adj_ptr, int32_t *adj,
                      int32_t *priorities);
+
+/* Multi-GPU, SURVEY.md §8(e) design M2: the valuation is replicated on every
+ * rank, the switch steps are sharded by vertex range (switchability is local to a
+ * vertex), and the switch lists are exchanged once per step.
+ *
+ * pg_allgather_fn: a collective all-gather supplied by the caller (e.g.
+ * torch.distributed over NCCL). Every rank calls it with the same `bytes`; it
+ * must gather `bytes` from each rank's `send` into `recv` (world*bytes, in rank
+ * order) and have completed when it returns (data visible to any stream).
+ * on_device = 1: send/recv are device pointers on the handle's device;
+ * 0: host pointers. Returns 0 on success, nonzero on failure. */
+typedef int (*pg_allgather_fn)(void *ctx, const void *send, void *recv, int64_t bytes,
+                               int32_t on_device);
+
+/* pg_dist_attach: make the handle one of `world` ranks solving the SAME game
+ * (every rank pg_load-s identical inputs with identical flags and then makes the
+ * same sequence of calls, collectively). Rank r evaluates All_Odd / All_Even only
+ * for its contiguous shard of the Odd and of the Even vertex range; after each
+ * switch step the ranks all-gather their (vertex, successor) switch lists and
+ * apply the union, so every rank holds the same profile and every result
+ * (winners, strategies, valuations, iteration counts) is identical to world = 1.
+ *   rank, world   0 <= rank < world; world = 1 or fn = NULL detaches
+ *   fn, ctx       the all-gather above; ctx is passed through and not owned
+ * Errors: PG_EINVAL (bad rank/world). A failing fn makes the next call return
+ * PG_ENCCL. */
+pg_status pg_dist_attach(pg_game g, int32_t rank, int32_t world, pg_allgather_fn fn,
+                         void *ctx);
 
 /* pg_get_stats: statistics of the last call on the handle (host pointer). */
 pg_status pg_get_stats(pg_game g, pg_stats *stats);

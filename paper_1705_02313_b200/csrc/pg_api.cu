@@ -56,6 +56,13 @@ struct pg_game_s {
     int64_t inc_s_div = 64;           // incremental step when |S| * inc_s_div <= n'
     int64_t last_maxdepth = 0;        // deepest play of the last full valuation
     uint32_t cepoch = 0;
+    // multi-GPU switch sharding (pg_dist_attach)
+    pg_allgather_fn dist_fn = nullptr;
+    void *dist_ctx = nullptr;
+    int32_t dist_rank = 0, dist_world = 1;
+    int2 *swl_all = nullptr;          // world × max(|S_r|) gathered switch lists
+    size_t swl_all_cap = 0;
+    int64_t *h_x = nullptr;           // pinned scratch (exchange counts, total |S|)
 };
 
 #define CK(h, x)                                                                         \
@@ -282,6 +289,58 @@ void note_valuation(pg_game h, bool full_rows, bool inc, bool bfs = false) {
     h->st.walk_steps += (int64_t)h->h_ctl->walk_steps;
 }
 
+// Sharded switch step: every rank evaluated only its shard and
+// recorded its switches in swl without applying them. All-gather the list sizes,
+// then the lists (padded to the largest), compact the union into swl (it is S of
+// the next incremental step on every rank) and apply it. The host copies of the
+// counters become the global ones, so every rank takes the same decisions.
+pg_status dist_exchange(pg_game h, bool odd) {
+    if (!h->dist_fn) return PG_OK;
+    const double t0 = now_ms();
+    const int W = h->dist_world;
+    std::vector<int64_t> all(W);
+    h->h_x[0] = (int64_t)h->h_ctl->nswl;
+    if (h->dist_fn(h->dist_ctx, h->h_x, all.data(), sizeof(int64_t), 0)) {
+        set_err("pg_dist_attach: all-gather callback failed (switch-list sizes)");
+        return PG_ENCCL;
+    }
+    int64_t maxc = 0, total = 0;
+    for (int r = 0; r < W; r++) { maxc = std::max(maxc, all[r]); total += all[r]; }
+    if (total > 0) {
+        const size_t need = (size_t)W * (size_t)maxc;
+        if (h->swl_all_cap < need) {
+            const size_t cap = std::min<size_t>((size_t)W * ((size_t)h->G.n_int + 1), std::max(need, 2 * h->swl_all_cap));
+            dfree(h, h->swl_all);
+            h->swl_all = nullptr;
+            h->swl_all_cap = 0;
+            CK(h, dalloc(h, &h->swl_all, cap));
+            h->swl_all_cap = cap;
+        }
+        if (h->dist_fn(h->dist_ctx, h->G.swl, h->swl_all, (int64_t)sizeof(int2) * maxc, 1)) {
+            set_err("pg_dist_attach: all-gather callback failed (switch lists)");
+            return PG_ENCCL;
+        }
+        int64_t off = 0;
+        for (int r = 0; r < W; r++) {
+            if (all[r]) CK(h, cudaMemcpyAsync(h->G.swl + off, h->swl_all + (size_t)r * maxc, sizeof(int2) * all[r],
+                                              cudaMemcpyDeviceToDevice, h->stream));
+            off += all[r];
+        }
+        h->h_x[1] = total;
+        CK(h, cudaMemcpyAsync(&h->G.ctl->nswl, &h->h_x[1], sizeof(int64_t), cudaMemcpyHostToDevice, h->stream));
+        CK(h, launch_apply_all(h->G, h->stream));
+        h->st.gpu_launches += 1;
+        CK(h, cudaStreamSynchronize(h->stream));   // h_x is reused by the next exchange
+        h->st.dist_bytes += (int64_t)sizeof(int2) * maxc;
+    }
+    h->h_ctl->nswl = (unsigned long long)total;
+    if (odd) h->h_ctl->odd_switches = (unsigned long long)total;
+    else h->h_ctl->even_switches = (unsigned long long)total;
+    h->st.dist_exchanges++;
+    h->st.ms_dist += now_ms() - t0;
+    return PG_OK;
+}
+
 // Incremental valuation pays off when the last switch step changed few choices.
 bool use_inc(pg_game h) {
     return h->have_state && h->G.dp <= 32 && h->last_nsw > 0 && !(h->flags & PG_NO_INCREMENTAL) &&
@@ -320,6 +379,10 @@ pg_status valuate_and_switch(pg_game h, bool odd, bool want_cdom, bool do_switch
         }
         if (!h->h_ctl->spl_overflow) break;
         rc = grow_splitters(h, (int64_t)h->h_ctl->nspl);   // rare: redo with larger buffers
+        if (rc) return rc;
+    }
+    if (do_switch) {
+        pg_status rc = dist_exchange(h, odd);
         if (rc) return rc;
     }
     h->have_state = true;
@@ -390,6 +453,7 @@ pg_status even_switch(pg_game h, int64_t *count) {
     }
     pg_status rc = readback(h);
     if (rc) return rc;
+    if ((rc = dist_exchange(h, false))) return rc;
     *count = (int64_t)h->h_ctl->even_switches;
     h->last_nsw = (int64_t)h->h_ctl->nswl;
     if (h->trace) fprintf(stderr, "[pgsi] even switch: inc=%d |C|=%llu |E|=%llu %lld switches\n", (int)inc,
@@ -504,6 +568,7 @@ void pg_free(pg_game h) {
     }
     if (h->stream) cudaStreamSynchronize(h->stream);
     if (h->h_ctl) cudaFreeHost(h->h_ctl);
+    if (h->h_x) cudaFreeHost(h->h_x);
     for (auto e : h->ev_pool) cudaEventDestroy(e);
     if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
     delete h;
@@ -666,6 +731,11 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
         CKL(dalloc(h, &G.sacc[1], (size_t)cap * dp));
         G.spl_cap = cap;
     }
+    G.sh_even_lo = 0;
+    G.sh_even_hi = L.n_even;
+    G.sh_odd_lo = L.n_even;
+    G.sh_odd_hi = L.n_int;
+    G.sharded = 0;
     CKL(launch_init_profile(G, s));
     CKL(cudaStreamSynchronize(s));
 #undef CKL
@@ -714,6 +784,40 @@ pg_status pg_inspect(int64_t n, const int64_t *row_ptr, const int32_t *col, cons
         }
     }
     if (adj_ptr) adj_ptr[H.n_int] = o;
+    return PG_OK;
+}
+
+pg_status pg_dist_attach(pg_game h, int32_t rank, int32_t world, pg_allgather_fn fn, void *ctx) {
+    pg_status rc = check_handle(h);
+    if (rc) return rc;
+    if (world < 1 || rank < 0 || rank >= world) { set_err("pg_dist_attach: need 0 <= rank < world"); return PG_EINVAL; }
+    DevGame &G = h->G;
+    auto span = [&](int64_t lo, int64_t n, int64_t &a, int64_t &b) {   // balanced contiguous shard
+        const int64_t q = n / world, r = n % world;
+        a = lo + rank * q + std::min<int64_t>(rank, r);
+        b = a + q + (rank < r ? 1 : 0);
+    };
+    if (world == 1 || !fn) {
+        h->dist_fn = nullptr;
+        h->dist_ctx = nullptr;
+        h->dist_rank = 0;
+        h->dist_world = 1;
+        G.sh_even_lo = 0; G.sh_even_hi = G.n_even;
+        G.sh_odd_lo = G.n_even; G.sh_odd_hi = G.n_int;
+        G.sharded = 0;
+        return PG_OK;
+    }
+    if (!h->h_x) {
+        DeviceGuard dg(h->device);
+        CK(h, cudaMallocHost((void **)&h->h_x, 4 * sizeof(int64_t)));
+    }
+    h->dist_fn = fn;
+    h->dist_ctx = ctx;
+    h->dist_rank = rank;
+    h->dist_world = world;
+    span(0, G.n_even, G.sh_even_lo, G.sh_even_hi);
+    span(G.n_even, G.n_int - G.n_even, G.sh_odd_lo, G.sh_odd_hi);
+    G.sharded = 1;
     return PG_OK;
 }
 

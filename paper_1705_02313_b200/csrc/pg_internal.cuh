@@ -114,6 +114,11 @@ struct DevGame {
     const int32_t *iperm;  // device -> ABI
     const int32_t *proj;   // device -> ABI id with dummies projected to their vertex
     Ctl *ctl;
+    // switch shard of this rank (pg_dist_attach); whole ranges
+    // when world = 1. sharded = 1: the switch kernels record S but do not apply it
+    // (the host exchanges the lists first and applies their union).
+    int64_t sh_even_lo, sh_even_hi, sh_odd_lo, sh_odd_hi;
+    int32_t sharded;
 };
 
 struct LaunchCfg {
@@ -136,6 +141,7 @@ cudaError_t launch_cycle_dom(const DevGame &g, const LaunchCfg &lc, cudaStream_t
 cudaError_t launch_switch(const DevGame &g, bool odd, cudaStream_t s);
 cudaError_t launch_inc_iter(const DevGame &g, const LaunchCfg &lc, cudaStream_t s, int64_t nS);
 cudaError_t launch_even_inc(const DevGame &g, cudaStream_t s);
+cudaError_t launch_apply_all(const DevGame &g, cudaStream_t s);   // σ[S]/τ[S] of the exchanged S
 cudaError_t launch_val_bfs(const DevGame &g, const LaunchCfg &lc, cudaStream_t s);
 size_t children_scan_bytes(int64_t n1);
 cudaError_t launch_export_val(const DevGame &g, int64_t count, int32_t *val_out, uint8_t *top_out,

@@ -851,6 +851,11 @@ __device__ __noinline__ int cmp_full(const DevGame &g, int32_t a, int32_t b) {
     return 0;
 }
 
+// Vertex v is in this rank's switch shard (always true when world = 1).
+__device__ __forceinline__ bool sh_owns(const DevGame &g, int64_t v) {
+    return v < g.n_even ? (v >= g.sh_even_lo && v < g.sh_even_hi) : (v >= g.sh_odd_lo && v < g.sh_odd_hi);
+}
+
 // One vertex of All_Odd / All_Even. HARD = false: compact prefixes only; a vertex
 // meeting an undecided comparison is appended to the hard list and left
 // unchanged. HARD = true: the hard list, resolving ties with cmp_full.
@@ -927,8 +932,9 @@ __device__ __forceinline__ int switch_vertex(const DevGame &g, int64_t v, const 
     return 0;
 }
 
-__global__ void k_apply_switches(DevGame g) {
+__global__ void k_apply_switches(DevGame g, int force) {
     if (__ldcg(&g.ctl->bfs_abort)) return;
+    if (g.sharded && !force) return;   // sharded: applied after the exchange (launch_apply_all)
     const int64_t cnt = (int64_t)__ldcg(&g.ctl->nswl);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cnt;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -941,14 +947,15 @@ template <bool ODD, bool HARD>
 __global__ void __launch_bounds__(kThreads) k_switch(DevGame g, const int32_t *vlist) {
     if (__ldcg(&g.ctl->spl_overflow) || __ldcg(&g.ctl->inc_overflow) || __ldcg(&g.ctl->bfs_abort)) return;
     const bool lst = vlist != nullptr;
-    const int64_t lo = (HARD || lst) ? 0 : (ODD ? g.n_even : 0);
+    const int64_t lo = (HARD || lst) ? 0 : (ODD ? g.sh_odd_lo : g.sh_even_lo);
     const int64_t hi = HARD ? (int64_t)__ldcg(&g.ctl->nhard)
-                            : (lst ? (int64_t)__ldcg(&g.ctl->nE) : (ODD ? g.n_int : g.n_even));
+                            : (lst ? (int64_t)__ldcg(&g.ctl->nE) : (ODD ? g.sh_odd_hi : g.sh_even_hi));
     const uint4 *cpx = reinterpret_cast<const uint4 *>(g.cpx);
     unsigned long long nsw = 0, reads = 0, fulls = 0;
     for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hi;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t v = HARD ? (int64_t)__ldcg(g.hard + i) : (lst ? (int64_t)__ldcg(vlist + i) : i);
+        if (lst && g.sharded && !sh_owns(g, v)) continue;   // another rank's vertex
         const int r = switch_vertex<ODD, HARD>(g, v, cpx, reads, fulls);
         if (r == 1) nsw++;
         if constexpr (!HARD) {
@@ -1202,6 +1209,7 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
     if (!ovf) {
         for (int64_t i = tid; i < ne; i += stride) {
             const int64_t v = __ldcg(g.El + i);
+            if (g.sharded && !sh_owns(g, v)) continue;   // another rank's vertex
             const int rr = switch_vertex<true, false>(g, v, cpx, reads, fulls);
             if (rr == 1) nsw++;
             else if (rr == 2) g.hard[atomicAdd(&ctl->nhard, 1ull)] = (int32_t)v;
@@ -1216,8 +1224,8 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
         }
     }
     gbar(ctl);
-    const int64_t nsl = (int64_t)*(volatile unsigned long long *)&ctl->nswl;
-    for (int64_t i = tid; i < nsl; i += stride) {
+    const int64_t nsl = g.sharded ? 0 : (int64_t)*(volatile unsigned long long *)&ctl->nswl;
+    for (int64_t i = tid; i < nsl; i += stride) {   // sharded: applied after the exchange
         const int2 e = __ldcg(g.swl + i);
         g.succ[e.x] = e.y;
     }
@@ -1619,7 +1627,7 @@ cudaError_t launch_switch(const DevGame &g, bool odd, cudaStream_t s) {
     else k_switch<false, true><<<hgrid, kThreads, 0, s>>>(g, nullptr);
     e = cudaGetLastError();
     if (e) return e;
-    k_apply_switches<<<std::max(1, g_lc.sms * 4), kThreads, 0, s>>>(g);
+    k_apply_switches<<<std::max(1, g_lc.sms * 4), kThreads, 0, s>>>(g, 0);
     return cudaGetLastError();
 }
 
@@ -1642,6 +1650,11 @@ cudaError_t launch_val_bfs(const DevGame &g, const LaunchCfg &lc, cudaStream_t s
     return cudaLaunchCooperativeKernel((const void *)k_val_bfs, dim3((unsigned)lc.coop_bfs), dim3(kThreads), args, 0, s);
 }
 
+cudaError_t launch_apply_all(const DevGame &g, cudaStream_t s) {
+    k_apply_switches<<<std::max(1, g_lc.sms * 4), kThreads, 0, s>>>(g, 1);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_even_inc(const DevGame &g, cudaStream_t s) {
     cudaError_t e = cudaMemsetAsync(&g.ctl->nhard, 0, 2 * sizeof(unsigned long long), s);  // nhard, nswl
     if (e) return e;
@@ -1651,7 +1664,7 @@ cudaError_t launch_even_inc(const DevGame &g, cudaStream_t s) {
     k_ebuild_even<<<grid, kThreads, 0, s>>>(g);
     k_switch<false, false><<<grid, kThreads, 0, s>>>(g, g.El);
     k_switch<false, true><<<std::max(1, g_lc.sms * 2), kThreads, 0, s>>>(g, nullptr);
-    k_apply_switches<<<grid, kThreads, 0, s>>>(g);
+    k_apply_switches<<<grid, kThreads, 0, s>>>(g, 0);
     return cudaGetLastError();
 }
 

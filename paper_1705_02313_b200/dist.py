@@ -1,9 +1,15 @@
 """Multi-GPU plumbing (torch.distributed).
 
-One process per GPU. The path is sharded by *problem*: every rank solves its own
-independent game (weak scaling), so there is no data-path collective. The only
-collectives are the bench's max-over-ranks timing and the sum of processed
-valuations. Works with the ``nccl`` backend on GPUs and ``gloo`` on CPU (tests).
+One process per GPU, two modes:
+
+- replicas (default bench): every rank solves its own independent game (weak
+  scaling); the only collectives are the bench's max-over-ranks timing and the
+  sum of processed valuations;
+- sharded (``pg_dist_attach``): all ranks solve ONE game,
+  the valuation is replicated and the switch steps are split by vertex range;
+  the per-step switch lists travel through :func:`torch_allgather`.
+
+Works with the ``nccl`` backend on GPUs and ``gloo`` on CPU (tests).
 """
 from __future__ import annotations
 
@@ -58,6 +64,54 @@ def reduce_time_and_units(dist, ms: float, units: float, device=None) -> Tuple[f
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     dist.all_reduce(u, op=dist.ReduceOp.SUM)
     return float(t.item()), float(u.item())
+
+
+class _CudaBuf:
+    """A raw device pointer exposed through ``__cuda_array_interface__``."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+def device_view(ptr: int, nbytes: int, device: int):
+    """uint8 torch view of nbytes of device memory at ptr (no copy)."""
+    import torch
+    return torch.as_tensor(_CudaBuf(ptr, nbytes), device=f"cuda:{device}")
+
+
+def host_view(ptr: int, nbytes: int):
+    """uint8 torch view of nbytes of host memory at ptr (no copy)."""
+    import ctypes
+    import torch
+    return torch.frombuffer((ctypes.c_uint8 * nbytes).from_address(ptr), dtype=torch.uint8)
+
+
+def torch_allgather(dist, device: int = 0):
+    """The all-gather ``Game.attach_dist`` needs, over the default process group:
+    NCCL gathers device tensors, gloo host tensors; buffers on the other side are
+    staged. Returns only after the data has landed (synchronises the device)."""
+    import torch
+    world = dist.get_world_size()
+    on_gpu_backend = dist.get_backend() == "nccl"
+
+    def allgather(send: int, recv: int, nbytes: int, on_device: bool) -> None:
+        if nbytes == 0:
+            return
+        src = device_view(send, nbytes, device) if on_device else host_view(send, nbytes)
+        dst = device_view(recv, nbytes * world, device) if on_device else host_view(recv, nbytes * world)
+        s = src
+        if on_gpu_backend and not on_device:
+            s = src.to(f"cuda:{device}")
+        elif not on_gpu_backend and on_device:
+            s = src.cpu()
+        parts = [torch.empty_like(s) for _ in range(world)]
+        dist.all_gather(parts, s)
+        dst.copy_(torch.cat(parts))
+        if on_device or on_gpu_backend:
+            torch.cuda.synchronize(device)
+
+    return allgather
 
 
 def barrier(dist) -> None:

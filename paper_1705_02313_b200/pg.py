@@ -60,11 +60,15 @@ class Stats(C.Structure):
         ("n_bfs", C.c_int64), ("bytes_bfs", C.c_double),
         ("dirty_vertices", C.c_int64),
         ("ms_inc", C.c_double),
-        ("n_inc", C.c_int64), ("bytes_inc", C.c_double)]
+        ("n_inc", C.c_int64), ("bytes_inc", C.c_double),
+        ("dist_exchanges", C.c_int64), ("dist_bytes", C.c_int64), ("ms_dist", C.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
+
+# int (*)(void *ctx, const void *send, void *recv, int64_t bytes, int32_t on_device)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32)
 
 _lib = None
 
@@ -85,8 +89,9 @@ def load_library(path: str = LIB_PATH):
     L.pg_solve.argtypes = [C.c_void_p, P, P, P, P, C.POINTER(Stats)]
     L.pg_get_stats.argtypes = [C.c_void_p, C.POINTER(Stats)]
     L.pg_inspect.argtypes = [C.c_int64, P, P, P, P, C.c_uint32] + [P] * 9
+    L.pg_dist_attach.argtypes = [C.c_void_p, C.c_int32, C.c_int32, ALLGATHER_FN, P]
     for f in ("pg_load", "pg_info", "pg_valuate", "pg_best_response", "pg_solve", "pg_get_stats",
-              "pg_inspect"):
+              "pg_inspect", "pg_dist_attach"):
         getattr(L, f).restype = C.c_int
     L.pg_free.argtypes = [C.c_void_p]
     L.pg_free.restype = None
@@ -175,6 +180,29 @@ class Game:
         if self.device_ptrs:
             return a
         return np.ascontiguousarray(a, dtype)
+
+    def attach_dist(self, rank: int, world: int, allgather=None):
+        """Make this handle rank `rank` of `world` ranks solving the same game with
+        range-sharded switch steps (``pg_dist_attach``).
+        ``allgather(send_ptr, recv_ptr, nbytes, on_device)`` must gather nbytes from
+        every rank into recv (rank order) and return when done, raising on failure
+        (see ``paper_1705_02313_b200.dist.torch_allgather``). world = 1 detaches."""
+        if allgather is None or world == 1:
+            self._dist_cb = None
+            self._check(_lib.pg_dist_attach(self._h, int(rank), int(world), ALLGATHER_FN(), None))
+            return
+
+        def cb(_ctx, send, recv, nbytes, on_device):
+            try:
+                allgather(int(send or 0), int(recv or 0), int(nbytes), bool(on_device))
+                return 0
+            except BaseException as e:   # noqa: BLE001 - reported through the C status
+                self.dist_error = e
+                return 1
+
+        self._dist_cb = ALLGATHER_FN(cb)   # keep the trampoline alive with the handle
+        self.dist_error = None
+        self._check(_lib.pg_dist_attach(self._h, int(rank), int(world), self._dist_cb, None))
 
     def stats(self) -> dict:
         s = Stats()

@@ -19,6 +19,7 @@ from .games import (  # noqa: F401
     f_oddchain,
     ladder,
     hanoi,
+    elevator,
     fixture_g2,
     from_adjacency,
     pgsolver_text,

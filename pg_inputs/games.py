@@ -234,6 +234,50 @@ def hanoi(k: int) -> Game:
     return _finish(deg, cand, owner, pri, f"hanoi-{k}")
 
 
+def elevator(f: int, r: int, seed: int) -> Game:
+    """SURVEY.md §8(d) config 4 family Elevator-(f, r), an elevator-like scheduler
+    product with d = 3 (Table 1's Elevator). The car is on floor
+    c in [0, f); floors 0..r-1 (r <= f) carry a pending-request bit in mask.
+
+    - Even (controller) vertex (c, mask), id = c*2^r + mask: moves the car up
+      or down, or serves the pending request on its floor. Priority 1 while the
+      request at the car's floor is pending, else 0.
+    - Odd (environment) vertex (s, c, mask), id = f*2^r + (s*f + c)*2^r + mask,
+      s = 1 right after a serve: passes, or adds the request j = H(seed, 11, id)
+      mod r when it is not already pending. Priority 2 on serve (s = 1), else 0.
+
+    3·f·2^r vertices (f = 20, r = 15 -> 1.97M), out-degree 1-3."""
+    assert f >= 2 and 1 <= r <= f
+    R = 1 << r
+    E = f * R
+    n = 3 * E
+    c = np.repeat(np.arange(f, dtype=np.int64), R)
+    mask = np.tile(np.arange(R, dtype=np.int64), f)
+    bit = np.where(c < r, np.left_shift(1, np.minimum(c, r - 1)), 0)
+    pending = (mask & bit) != 0
+    cand = np.full((n, 3), -1, dtype=np.int64)
+    deg = np.zeros(n, dtype=np.int64)
+    ev = np.arange(E, dtype=np.int64)
+
+    def push(rows, tgt, ok):
+        idx = rows[ok]
+        cand[idx, deg[idx]] = tgt[ok]
+        deg[idx] += 1
+
+    push(ev, E + (c + 1) * R + mask, c + 1 < f)                   # up
+    push(ev, E + (c - 1) * R + mask, c > 0)                       # down
+    push(ev, E + (f + c) * R + (mask & ~bit), pending)            # serve -> s = 1
+    for s_ in range(2):
+        ov = E + s_ * E + ev
+        push(ov, ev, np.ones(E, bool))                            # pass
+        j = (counter_hash(seed, 11, ov.astype(_U64), np.zeros(E, _U64)) % _U64(r)).astype(np.int64)
+        req = np.left_shift(1, j)
+        push(ov, c * R + (mask | req), (mask & req) == 0)         # new request
+    owner = np.concatenate([np.zeros(E, np.uint8), np.ones(2 * E, np.uint8)])
+    pri = np.concatenate([np.where(pending, 1, 0), np.zeros(E), np.full(E, 2)]).astype(np.int32)
+    return _finish(deg, cand, owner, pri, f"elevator-{f}-{r}-s{seed}")
+
+
 def pgsolver_text(g: Game) -> str:
     """Serialise in the PGSolver format (SPEC.md game_core interface idea)."""
     lines = [f"parity {g.n - 1};"]

@@ -1,0 +1,17 @@
+#!/bin/bash
+# Profiling pass for profiles/<round>/ (run under gpurun on one B200).
+#  1. bench line (CUDA events, not under a profiler)
+#  2. ncu launch list of one config-3 solve (cold-cache, serialised: compare shares)
+#  3. ncu --set full of one mid-solve launch of each top kernel
+set -u
+OUT=gpurun_out/prof
+mkdir -p $OUT
+timeout -k 5 300 python bench.py --steps 5 --warmup 3 > $OUT/bench.json 2> $OUT/bench.err
+M=gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sector_hit_rate.pct,smsp__inst_executed.sum
+timeout -k 5 600 ncu --metrics $M --clock-control none -c 3000 --csv --log-file $OUT/launches.csv \
+    python bench.py --profile --steps 1 --warmup 0 > $OUT/launches.log 2>&1
+for k in k_inc_iter k_v2_cpx k_switch k_v1; do
+  timeout -k 5 600 ncu --set full --clock-control none --import-source on -k regex:"^${k}\$" -s 8 -c 1 \
+      -o $OUT/full_$k python bench.py --profile --steps 1 --warmup 0 > $OUT/full_$k.log 2>&1
+done
+ls -la $OUT

@@ -69,7 +69,7 @@ def test_host_transform_matches_oracle_random(pgmod, seed):
 
 
 def test_host_transform_matches_oracle_structured(pgmod):
-    for g in (gi.ladder(2000, 3), gi.hanoi(5), gi.f_deep(50), gi.f_oddchain(20), gi.f_stair(9),
+    for g in (gi.ladder(2000, 3), gi.hanoi(5), gi.elevator(5, 4, 2), gi.f_deep(50), gi.f_oddchain(20), gi.f_stair(9),
               gi.fixture_g2(), gi.from_adjacency([1], [3], [[0]])):
         _compare_internal(pgmod, g)
 

@@ -30,7 +30,13 @@ def _worker(rank, world, port, q):
     pgdist.barrier(d)
     import pg_inputs as gi
     g = gi.random_game(50, 4, 1, 3, pgdist.game_seed(7, r))
-    q.put((r, w, lr, t, u, int(g.col.sum())))
+    # the switch-list all-gather adapter (pg_dist_attach) on host buffers
+    import ctypes
+    ag = pgdist.torch_allgather(d)
+    send = (ctypes.c_int64 * 3)(10 * rank + 1, 10 * rank + 2, -rank)
+    recv = (ctypes.c_int64 * 6)()
+    ag(ctypes.addressof(send), ctypes.addressof(recv), 24, False)
+    q.put((r, w, lr, t, u, int(g.col.sum()), list(recv)))
     d.destroy_process_group()
 
 
@@ -48,6 +54,7 @@ def test_gloo_world2_reductions_and_seeds():
     assert all(r[3] == 20.0 for r in res)            # max over ranks
     assert all(r[4] == 2001.0 for r in res)          # sum over ranks
     assert res[0][5] != res[1][5]                    # independent games per rank
+    assert all(r[6] == [1, 2, 0, 11, 12, -1] for r in res)   # rank-ordered all-gather
 
 
 def test_single_process_is_noop():

@@ -188,11 +188,12 @@ def test_solve_random_shapes(pg, n, d, lo, hi, seed):
     assert_solve_equal(res, ora, n, G.d)
 
 
-@pytest.mark.parametrize("name", ["stair", "deep", "oddchain", "ladder", "hanoi", "g2", "selfloops"])
+@pytest.mark.parametrize("name", ["stair", "deep", "oddchain", "ladder", "hanoi", "elevator", "g2",
+                                  "selfloops"])
 def test_solve_structured(pg, name):
     g = {"stair": lambda: gi.f_stair(300), "deep": lambda: gi.f_deep(100000),
          "oddchain": lambda: gi.f_oddchain(200), "ladder": lambda: gi.ladder(60000, 2),
-         "hanoi": lambda: gi.hanoi(8), "g2": gi.fixture_g2,
+         "hanoi": lambda: gi.hanoi(8), "elevator": lambda: gi.elevator(8, 8, 3), "g2": gi.fixture_g2,
          "selfloops": lambda: gi.from_adjacency([1, 0], [3, 2], [[0], [1]])}[name]()
     ora = Oracle(g).solve()
     G = pg.Game.from_game(g)
@@ -283,7 +284,7 @@ def test_incremental_matches_full_and_oracle(pg, n, d, seed):
 
 
 def test_incremental_structured_and_forced(pg):
-    for g in (gi.ladder(40000, 9), gi.hanoi(8), gi.f_oddchain(3000), gi.f_stair(400)):
+    for g in (gi.ladder(40000, 9), gi.hanoi(8), gi.elevator(10, 9, 4), gi.f_oddchain(3000), gi.f_stair(400)):
         ora = Oracle(g).solve()
         for pairs in (0, 1):
             G = pg.Game.from_game(g, prefix_pairs=pairs)

@@ -320,7 +320,7 @@ def test_pgsolver_roundtrip():
 
 
 def test_structured_families_solve():
-    for g in (gi.ladder(400, 1), gi.hanoi(4)):
+    for g in (gi.ladder(400, 1), gi.hanoi(4), gi.elevator(3, 2, 1), gi.elevator(4, 3, 5)):
         r = Oracle(g).solve()
         owner, prio, adj = _orig(g)
         if g.n <= 200:
