@@ -393,6 +393,12 @@ pg_status valuate_and_switch(pg_game h, bool odd, bool want_cdom, bool do_switch
         fprintf(stderr, "[pgsi] valuation %.3f ms inc=%d nD=%llu lev=%llu rounds=%llu steps=%llu nE=%llu switches=%llu hard=%llu\n",
                 now_ms() - t_start, (int)inc, h->h_ctl->nD, h->h_ctl->dlevels, h->h_ctl->v1_rounds, h->h_ctl->walk_steps,
                 h->h_ctl->nE, h->h_ctl->nswl, h->h_ctl->nhard);
+    if (h->trace && inc && h->G.trace_ts) {
+        const unsigned long long *t = h->h_ctl->ts;
+        fprintf(stderr, "[pgsi]   inc phases (us): closure %.1f  C %.1f  V1 %.1f  V2 %.1f  E %.1f  switch %.1f  hard %.1f  apply %.1f\n",
+                (t[1] - t[0]) * 1e-3, (t[2] - t[1]) * 1e-3, (t[3] - t[2]) * 1e-3, (t[4] - t[3]) * 1e-3,
+                (t[5] - t[4]) * 1e-3, (t[6] - t[5]) * 1e-3, (t[7] - t[6]) * 1e-3, (t[8] - t[7]) * 1e-3);
+    }
     note_valuation(h, !do_switch, inc, bfs);
     h->last_inc = inc;
     return PG_OK;
@@ -587,7 +593,8 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     h->device = o.device;
     h->flags = o.flags;
     h->max_inner = o.max_inner;
-    h->trace = getenv("PGSI_TRACE") && getenv("PGSI_TRACE")[0] == '1';
+    h->trace = getenv("PGSI_TRACE") && (getenv("PGSI_TRACE")[0] == '1' || getenv("PGSI_TRACE")[0] == '2');
+    h->G.trace_ts = getenv("PGSI_TRACE") && getenv("PGSI_TRACE")[0] == '2';
     h->max_outer = o.max_outer;
     DeviceGuard dg(h->device);
     auto fail = [&](pg_status r) { pg_free(h); return r; };

@@ -65,6 +65,7 @@ struct Ctl {
     unsigned long long nC;          // |C|: vertices in some dirty set since the last All_Even
     unsigned int bar_count;         // grid barrier
     unsigned int bar_gen;
+    unsigned long long ts[12];      // PGSI_TRACE=2: %globaltimer at the incremental kernel's phase ends
 };
 #define PGSI_CTL_RESET_BYTES offsetof(pgsi::Ctl, bad_index)
 
@@ -119,6 +120,7 @@ struct DevGame {
     // (the host exchanges the lists first and applies their union).
     int64_t sh_even_lo, sh_even_hi, sh_odd_lo, sh_odd_hi;
     int32_t sharded;
+    int32_t trace_ts;   // PGSI_TRACE=2: record phase timestamps in ctl->ts
 };
 
 struct LaunchCfg {

@@ -38,6 +38,17 @@ __device__ __forceinline__ unsigned long long pack_jl(uint32_t J, uint32_t len) 
 // hand-rolled atomic barrier; scripts/micro/barrier_bench.cu).
 __device__ __forceinline__ void grid_barrier(Ctl *) { cooperative_groups::this_grid().sync(); }
 
+// A grid-wide counter read right after a grid barrier: one L2 load per block,
+// broadcast through shared memory (every thread reading the same word costs one
+// serialised L2 request per warp on a single slice). Block-uniform call sites only.
+__device__ __forceinline__ unsigned long long bcast_ld(const unsigned long long *p) {
+    __shared__ unsigned long long s;
+    __syncthreads();
+    if (threadIdx.x == 0) s = __ldcg(p);
+    __syncthreads();
+    return s;
+}
+
 template <typename T>
 __device__ __forceinline__ T block_sum(T x) {
     __shared__ T red[32];
@@ -147,8 +158,8 @@ __global__ void __launch_bounds__(kThreads) k_v1(DevGame g) {
     if (threadIdx.x == 0 && t) atomicAdd(&g.ctl->alen[1], t);
     grid_barrier(g.ctl);
     int r = 1;
-    bool go = *(volatile unsigned long long *)&g.ctl->newfin[1] != 0;
-    unsigned long long left = *(volatile unsigned long long *)&g.ctl->alen[1];
+    bool go = bcast_ld(&g.ctl->newfin[1]) != 0;
+    unsigned long long left = bcast_ld(&g.ctl->alen[1]);
     // in-place rounds; a round can only be needed while some vertex finishes, and
     // depth < 2^31 bounds the count (hard cap: no hang even on corrupt input)
     while (go && r < 64) {
@@ -180,8 +191,8 @@ __global__ void __launch_bounds__(kThreads) k_v1(DevGame g) {
         t = block_sum(act);
         if (threadIdx.x == 0 && t) atomicAdd(&g.ctl->alen[r % 3], t);
         grid_barrier(g.ctl);
-        go = *(volatile unsigned long long *)&g.ctl->newfin[r % 3] != 0;
-        left = *(volatile unsigned long long *)&g.ctl->alen[r % 3];
+        go = bcast_ld(&g.ctl->newfin[r % 3]) != 0;
+        left = bcast_ld(&g.ctl->alen[r % 3]);
         if (blockIdx.x == 0 && threadIdx.x == 0) {   // counters of round r+2 (never touched yet)
             g.ctl->newfin[(r + 2) % 3] = 0;
             g.ctl->alen[(r + 2) % 3] = 0;
@@ -730,7 +741,7 @@ __global__ void __launch_bounds__(kThreads) k_spl_wyllie(DevGame g) {
         unsigned long long tot = block_sum(local);
         if (threadIdx.x == 0 && tot) atomicAdd(&g.ctl->spl_active[r % 3], tot);
         grid_barrier(g.ctl);
-        unsigned long long act = *(volatile unsigned long long *)&g.ctl->spl_active[r % 3];
+        unsigned long long act = bcast_ld(&g.ctl->spl_active[r % 3]);
         if (blockIdx.x == 0 && threadIdx.x == 0) g.ctl->spl_active[(r + 2) % 3] = 0;
         cur = nx;
         r++;
@@ -1056,6 +1067,14 @@ __device__ __forceinline__ void expand_rev(const DevGame &g, int32_t f, uint32_t
     }
 }
 
+__device__ __forceinline__ void trace_ts(const DevGame &g, int k) {
+    if (g.trace_ts && blockIdx.x == 0 && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g.ctl->ts[k] = t;
+    }
+}
+
 __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
     __shared__ uint8_t hsm[kThreads][36];
     __shared__ uint32_t osm[kThreads][9];
@@ -1068,6 +1087,7 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
     const int64_t wbase = tid - lane;
     Ctl *ctl = g.ctl;
 
+    trace_ts(g, 0);
     // ---- 1. dirty closure
     const int64_t ns = (int64_t)__ldcg(&ctl->nswl);
     for (int64_t i = tid; i < ns; i += stride) {
@@ -1095,7 +1115,7 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
             expand_rev<0>(g, f, rb, re, g.dmark, ep, out, cnt);
         }
         gbar(ctl);
-        const int64_t added = (int64_t)*(volatile unsigned long long *)cnt;
+        const int64_t added = (int64_t)bcast_ld(cnt);
         if (blockIdx.x == 0 && threadIdx.x == 0) ctl->dcnt[(levels + 2) % 3] = 0;
         lo = hi;
         hi += added;
@@ -1107,6 +1127,7 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
         }
     }
     const int64_t nd = hi;
+    trace_ts(g, 1);
     // C ∪= D (every vertex whose valuation may have changed since the last All_Even)
     for (int64_t b0 = wbase; b0 < nd; b0 += stride) {
         const int64_t i = b0 + lane;
@@ -1117,6 +1138,7 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
     }
 
     // ---- 2. V1 on D
+    trace_ts(g, 2);
     unsigned long long *jl = g.jl;
     for (int64_t i = tid; i < nd; i += stride) {
         const int32_t v = __ldcg(g.Dl + i);
@@ -1153,11 +1175,12 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
         nf = block_sum(nf);
         if (threadIdx.x == 0 && nf) atomicAdd(&ctl->newfin[r % 3], nf);
         gbar(ctl);
-        go = *(volatile unsigned long long *)&ctl->newfin[r % 3] != 0;
+        go = bcast_ld(&ctl->newfin[r % 3]) != 0;
         if (blockIdx.x == 0 && threadIdx.x == 0) ctl->newfin[(r + 2) % 3] = 0;
     }
 
     // ---- 3. V2 on D
+    trace_ts(g, 3);
     uint8_t *hb = hsm[threadIdx.x];
     uint32_t *ow = osm[threadIdx.x];
 #pragma unroll
@@ -1189,6 +1212,7 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
     gbar(ctl);
 
     // ---- 4. E = Odd vertices with a candidate in D
+    trace_ts(g, 4);
     for (int64_t b0 = wbase; b0 < nd; b0 += stride) {
         const int64_t i = b0 + lane;
         uint32_t rb = 0, re = 0;
@@ -1200,8 +1224,9 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
         expand_rev<1>(g, -1, rb, re, g.emark, ep, g.El, &ctl->nE);
     }
     gbar(ctl);
-    const int64_t ne = (int64_t)*(volatile unsigned long long *)&ctl->nE;
-    const bool ovf = *(volatile unsigned long long *)&ctl->inc_overflow != 0;
+    const int64_t ne = (int64_t)bcast_ld(&ctl->nE);
+    const bool ovf = bcast_ld(&ctl->inc_overflow) != 0;
+    trace_ts(g, 5);
 
     // ---- 5-7. All_Odd over E: prefix pass, hard pass, apply
     const uint4 *cpx = reinterpret_cast<const uint4 *>(g.cpx);
@@ -1216,15 +1241,17 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
         }
     }
     gbar(ctl);
+    trace_ts(g, 6);
     if (!ovf) {
-        const int64_t nh = (int64_t)*(volatile unsigned long long *)&ctl->nhard;
+        const int64_t nh = (int64_t)bcast_ld(&ctl->nhard);
         for (int64_t i = tid; i < nh; i += stride) {
             const int64_t v = __ldcg(g.hard + i);
             if (switch_vertex<true, true>(g, v, cpx, reads, fulls) == 1) nsw++;
         }
     }
     gbar(ctl);
-    const int64_t nsl = g.sharded ? 0 : (int64_t)*(volatile unsigned long long *)&ctl->nswl;
+    trace_ts(g, 7);
+    const int64_t nsl = g.sharded ? 0 : (int64_t)bcast_ld(&ctl->nswl);
     for (int64_t i = tid; i < nsl; i += stride) {   // sharded: applied after the exchange
         const int2 e = __ldcg(g.swl + i);
         g.succ[e.x] = e.y;
@@ -1242,6 +1269,7 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
         ctl->dlevels = (unsigned long long)levels;
         ctl->v1_rounds = (unsigned long long)r;
     }
+    trace_ts(g, 8);
 }
 
 
@@ -1378,7 +1406,7 @@ __global__ void __launch_bounds__(kThreads) k_val_bfs(DevGame g) {
         }
     }
     gbar(ctl);
-    int64_t len = (int64_t)*(volatile unsigned long long *)&ctl->dcnt[1];
+    int64_t len = (int64_t)bcast_ld(&ctl->dcnt[1]);
     int lev = 1;
     unsigned long long nfin = len;
     int32_t *cur = g.Dl, *nxt = g.El;
@@ -1425,7 +1453,7 @@ __global__ void __launch_bounds__(kThreads) k_val_bfs(DevGame g) {
             }
         }
         gbar(ctl);
-        len = (int64_t)*(volatile unsigned long long *)cnt;
+        len = (int64_t)bcast_ld(cnt);
         if (blockIdx.x == 0 && threadIdx.x == 0) ctl->dcnt[lev % 3] = 0;   // read one level ago
         nfin += (unsigned long long)len;
         lev++;
