@@ -54,6 +54,7 @@ struct pg_game_s {
     bool trace = false;               // PGSI_TRACE=1 (debug)
     bool c_valid = false;             // C covers every change since the last All_Even
     int64_t inc_s_div = 64;           // incremental step when |S| * inc_s_div <= n'
+    int64_t inc_max_steps = 1 << 20;  // inner iterations per incremental launch (PGSI_INC_STEPS)
     int64_t last_maxdepth = 0;        // deepest play of the last full valuation
     uint32_t cepoch = 0;
     // multi-GPU switch sharding (pg_dist_attach)
@@ -204,7 +205,8 @@ pg_status grow_splitters(pg_game h, int64_t need) {
 
 // One valuation of the current profile (σ ∪ τ in G.succ): V1 then V2.
 // inc = incremental (only D = upward closure of the last switch list, §V-inc).
-pg_status valuate_dev(pg_game h, bool want_cdom, bool full_rows, bool inc = false, bool bfs = false) {
+pg_status valuate_dev(pg_game h, bool want_cdom, bool full_rows, bool inc = false, bool bfs = false,
+                      int64_t max_steps = 1) {
     if (full_rows && !h->G.val) {   // full key rows are only needed for outputs: allocated lazily
         const size_t N1 = (size_t)h->G.n_int + 1;
         CK(h, dalloc(h, &h->G.val, N1 * h->G.dp));
@@ -219,12 +221,16 @@ pg_status valuate_dev(pg_game h, bool want_cdom, bool full_rows, bool inc = fals
     }
     CK(h, cudaMemsetAsync(h->G.ctl, 0, PGSI_CTL_RESET_BYTES, h->stream));
     if (inc) {   // incremental valuation + All_Odd in one cooperative kernel (§V-inc)
-        h->G.epoch = ++h->epoch;
-        if (h->G.epoch == 0) {                       // wrapped: clear the marks
+        // up to max_steps inner iterations in this launch; step t marks with epoch + t
+        const uint32_t steps = (uint32_t)std::max<int64_t>(1, std::min<int64_t>(max_steps, 1 << 20));
+        if (h->epoch > 0xffffffffu - steps - 1) {    // would wrap: clear the marks
             CK(h, cudaMemsetAsync(h->G.dmark, 0, sizeof(uint32_t) * ((size_t)h->G.n_int + 1), h->stream));
             CK(h, cudaMemsetAsync(h->G.emark, 0, sizeof(uint32_t) * ((size_t)h->G.n_int + 1), h->stream));
-            h->G.epoch = ++h->epoch;
+            h->epoch = 0;
         }
+        h->G.epoch = h->epoch + 1;
+        h->epoch += steps;
+        h->G.inc_max_steps = (int32_t)steps;
         PhaseScope ps(h, PH_INC);
         CK(h, launch_inc_iter(h->G, h->lc, h->stream, h->last_nsw));
         h->st.gpu_launches += 1;
@@ -271,13 +277,18 @@ void note_valuation(pg_game h, bool full_rows, bool inc, bool bfs = false) {
         h->st.top_vertices += (int64_t)h->h_ctl->n_top;
         if ((int64_t)h->h_ctl->maxdepth > h->st.max_depth) h->st.max_depth = (int64_t)h->h_ctl->maxdepth;
         h->st.bfs_valuations++;
-    } else if (inc) {
-        const double nd = (double)h->h_ctl->nD;
-        h->st.inc_valuations++;
-        h->st.dirty_vertices += (int64_t)h->h_ctl->nD;
+    } else if (inc) {   // the completed steps of one k_inc_iter launch (sums over steps)
+        const double nd = (double)h->h_ctl->nD_sum, ne = (double)h->h_ctl->nE_sum;
+        h->st.inc_valuations += (int64_t)h->h_ctl->steps_done;
+        h->st.dirty_vertices += (int64_t)h->h_ctl->nD_sum;
         // per dirty vertex: reverse edges scanned with the predecessors' succ (≈ 8 B × in-degree),
-        // D list w+r, succ, jl w+r, pidx, ⊤, the exit vertex's prefix and its own prefix
-        h->st.bytes_inc += nd * (8.0 * h->avg_indeg + 8.0 + 4.0 + 16.0 + 1.0 + 1.0 + 32.0 + 32.0);
+        // D list + reverse range w+r, succ, jl w+r, pidx, ⊤, the exit vertex's prefix and its own
+        // prefix; per E vertex its list entry, mark, CSR range, successors and the prefix gathers
+        h->st.bytes_inc += nd * (8.0 * h->avg_indeg + 8.0 + 16.0 + 4.0 + 16.0 + 1.0 + 1.0 + 32.0 + 32.0) +
+                           4.0 * ne + 12.0 * ne + 4.0 * h->avg_indeg * ne + 32.0 * (double)h->h_ctl->rows_odd +
+                           8.0 * (double)h->h_ctl->odd_switches;
+        h->st.odd_switches += (int64_t)h->h_ctl->odd_switches;
+        h->st.full_compares += (int64_t)h->h_ctl->full_odd;
     } else {
         h->st.bytes_v1 += 5.0 * np_;
         h->st.bytes_v2 += np_ + (full_rows ? R * (double)h->h_ctl->n_fin : 32.0 * np_);
@@ -334,8 +345,12 @@ pg_status dist_exchange(pg_game h, bool odd) {
         h->st.dist_bytes += (int64_t)sizeof(int2) * maxc;
     }
     h->h_ctl->nswl = (unsigned long long)total;
-    if (odd) h->h_ctl->odd_switches = (unsigned long long)total;
-    else h->h_ctl->even_switches = (unsigned long long)total;
+    if (odd) {
+        h->h_ctl->odd_switches = (unsigned long long)total;
+        h->h_ctl->last_sw = (unsigned long long)total;   // sharded launches run one step
+    } else {
+        h->h_ctl->even_switches = (unsigned long long)total;
+    }
     h->st.dist_exchanges++;
     h->st.ms_dist += now_ms() - t0;
     return PG_OK;
@@ -347,17 +362,29 @@ bool use_inc(pg_game h) {
            !(h->flags & PG_CHECK_INVARIANTS) && h->last_nsw * h->inc_s_div <= h->G.n_int;
 }
 
-// valuation + one switch step; redone in full if the splitter buffers overflowed
-// or an incremental walk exceeded the byte counters (both rare).
-pg_status valuate_and_switch(pg_game h, bool odd, bool want_cdom, bool do_switch) {
+// Result of valuate_and_switch: valuations computed and the switches of the last
+// (and of all) switch steps among them.
+struct StepOut {
+    int64_t nval = 0;
+    int64_t sw_last = 0;
+};
+
+// valuation + switch step(s). An incremental launch may run up to max_steps inner
+// iterations on the device (k_inc_iter step 8). Redone in full when the splitter
+// buffers overflowed or an incremental step aborted (closure too deep / large).
+pg_status valuate_and_switch(pg_game h, bool odd, bool want_cdom, bool do_switch, StepOut *out = nullptr,
+                             int64_t max_steps = 1) {
     bool inc = do_switch && odd && !want_cdom && use_inc(h);
     // BFS valuation unless the last full valuation was too deep for it (then it would abort)
     const bool bfs_ok = do_switch && h->G.dp <= 32 && (h->flags & PG_BFS) &&
                         h->last_maxdepth * 4 < (int64_t)h->G.bfs_max_levels * 3;
     bool bfs = !inc && bfs_ok;
+    if (h->dist_fn || h->G.trace_ts) max_steps = 1;   // sharded: the host exchanges S every step
+    max_steps = std::min<int64_t>(max_steps, h->inc_max_steps);
     const double t_start = h->trace ? now_ms() : 0.0;
+    int64_t done_inc = 0;      // inner iterations completed by an incremental launch that then aborted
     for (;;) {
-        pg_status rc = valuate_dev(h, want_cdom, !do_switch, inc, bfs);
+        pg_status rc = valuate_dev(h, want_cdom, !do_switch, inc, bfs, max_steps);
         if (rc) return rc;
         if (do_switch && !inc) {
             PhaseScope ps(h, odd ? PH_ODD : PH_EVEN);
@@ -366,7 +393,13 @@ pg_status valuate_and_switch(pg_game h, bool odd, bool want_cdom, bool do_switch
         }
         rc = readback(h);
         if (rc) return rc;
-        if (h->h_ctl->inc_overflow) {   // closure too deep/large or walk too long: redo in full
+        if (h->h_ctl->inc_overflow) {   // closure too deep/large or walk too long: redo that step in full
+            if (h->h_ctl->steps_done) {  // the steps before it stand
+                done_inc = (int64_t)h->h_ctl->steps_done;
+                note_valuation(h, false, true);
+                if (h->trace)
+                    fprintf(stderr, "[pgsi] incremental launch: %lld steps, then abort\n", (long long)done_inc);
+            }
             inc = false;
             bfs = bfs_ok;
             h->st.inc_aborts++;
@@ -390,9 +423,10 @@ pg_status valuate_and_switch(pg_game h, bool odd, bool want_cdom, bool do_switch
     if (!inc) h->last_maxdepth = (int64_t)h->h_ctl->maxdepth;
     if (!inc) h->c_valid = false;   // a from-scratch valuation: C no longer covers the changes
     if (h->trace)
-        fprintf(stderr, "[pgsi] valuation %.3f ms inc=%d nD=%llu lev=%llu rounds=%llu steps=%llu nE=%llu switches=%llu hard=%llu\n",
-                now_ms() - t_start, (int)inc, h->h_ctl->nD, h->h_ctl->dlevels, h->h_ctl->v1_rounds, h->h_ctl->walk_steps,
-                h->h_ctl->nE, h->h_ctl->nswl, h->h_ctl->nhard);
+        fprintf(stderr, "[pgsi] valuation %.3f ms inc=%d steps=%llu nD=%llu lev=%llu rounds=%llu walk=%llu nE=%llu switches=%llu hard=%llu\n",
+                now_ms() - t_start, (int)inc, inc ? h->h_ctl->steps_done : 1ull, inc ? h->h_ctl->nD_sum : 0ull,
+                h->h_ctl->dlevels, h->h_ctl->v1_rounds, h->h_ctl->walk_steps,
+                inc ? h->h_ctl->nE_sum : h->h_ctl->nE, h->h_ctl->nswl, h->h_ctl->nhard);
     if (h->trace && inc && h->G.trace_ts) {
         const unsigned long long *t = h->h_ctl->ts;
         fprintf(stderr, "[pgsi]   inc phases (us): closure %.1f  C %.1f  V1 %.1f  V2 %.1f  E %.1f  switch %.1f  hard %.1f  apply %.1f\n",
@@ -401,6 +435,10 @@ pg_status valuate_and_switch(pg_game h, bool odd, bool want_cdom, bool do_switch
     }
     note_valuation(h, !do_switch, inc, bfs);
     h->last_inc = inc;
+    if (out) {
+        out->nval = done_inc + (inc ? (int64_t)h->h_ctl->steps_done : 1);
+        out->sw_last = inc ? (int64_t)h->h_ctl->last_sw : (int64_t)h->h_ctl->odd_switches;
+    }
     return PG_OK;
 }
 
@@ -411,26 +449,24 @@ pg_status inner_loop(pg_game h, int64_t *inner, bool check) {
             set_err("inner iteration cap reached");
             return PG_EITERCAP;
         }
-        pg_status rc = valuate_and_switch(h, true, check, true);
+        StepOut so;
+        const int64_t room = h->max_inner > 0 ? h->max_inner - *inner : INT64_MAX;
+        pg_status rc = valuate_and_switch(h, true, check, true, &so, room);
         if (rc) return rc;
-        (*inner)++;
+        *inner += so.nval;
         if (check && h->h_ctl->odd_cycle) {
             set_err("odd cycle reached: strategy not admissible");
             return PG_EINADMISSIBLE;
         }
-        int64_t c = (int64_t)h->h_ctl->odd_switches;
-        h->st.odd_switches += c;
-        if (h->last_inc) {   // All_Odd over E ran inside the incremental kernel
-            const double ne = (double)h->h_ctl->nE;
-            h->st.bytes_inc += 4.0 * ne + 12.0 * ne + 4.0 * h->avg_indeg * ne +
-                               32.0 * (double)h->h_ctl->rows_odd + 8.0 * c;
-        } else {
+        if (!h->last_inc) {   // from-scratch All_Odd (incremental steps are counted in note_valuation)
+            const int64_t c = (int64_t)h->h_ctl->odd_switches;
+            h->st.odd_switches += c;
             const double no = (double)(h->G.n_int - h->G.n_even), mo = (double)h->m_odd;
             h->st.bytes_odd += 4.0 * (no + 1) + 4.0 * no + 4.0 * mo + 32.0 * (double)h->h_ctl->rows_odd +
                                8.0 * h->G.dp * (double)h->h_ctl->full_odd + 4.0 * c;
+            h->st.full_compares += (int64_t)h->h_ctl->full_odd;
         }
-        h->st.full_compares += (int64_t)h->h_ctl->full_odd;
-        if (c == 0) return PG_OK;
+        if (so.sw_last == 0) return PG_OK;
     }
 }
 
@@ -707,6 +743,7 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     CKL(dalloc(h, &G.emark, N1));
     CKL(dalloc(h, &G.cmark, N1));
     CKL(dalloc(h, &G.Dl, N1));
+    CKL(dalloc(h, &G.Dr, N1));
     CKL(dalloc(h, &G.El, N1));
     CKL(dalloc(h, &G.Cl, N1));
     CKL(cudaMemsetAsync(G.dmark, 0, sizeof(uint32_t) * N1, s));
@@ -720,6 +757,10 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     G.bfs_max_levels = getenv("PGSI_BFS_MAX_LEVELS") ? atoi(getenv("PGSI_BFS_MAX_LEVELS")) : 160;
     G.inc_max_dirty = std::max<int64_t>(4096, L.n_int / (getenv("PGSI_INC_DIRTY_DIV") ? atoi(getenv("PGSI_INC_DIRTY_DIV")) : 8));
     h->inc_s_div = getenv("PGSI_INC_S_DIV") ? atoi(getenv("PGSI_INC_S_DIV")) : 64;
+    h->inc_max_steps = getenv("PGSI_INC_STEPS") ? std::max(1, atoi(getenv("PGSI_INC_STEPS"))) : (1 << 20);
+    G.inc_s_div = h->inc_s_div;
+    G.inc_grid_cap = h->lc.coop_inc;
+    G.inc_max_steps = 1;
     // children CSR scratch of the BFS valuation (§V-bfs)
     CKL(dalloc(h, &G.ccnt, N1));
     CKL(dalloc(h, &G.cptr, N1));

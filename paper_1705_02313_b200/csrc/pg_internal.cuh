@@ -58,6 +58,11 @@ struct Ctl {
     unsigned long long dlevels;     // BFS levels of the dirty closure
     unsigned long long dcnt[3];     // per-level append counters of the dirty BFS (rotating)
     unsigned long long bfs_abort;   // top-down BFS valuation exceeded bfs_max_levels
+    unsigned long long steps_done;  // incremental launch: inner iterations completed on the device
+    unsigned long long last_sw;     // ... switches of the last completed one (0 = converged)
+    unsigned long long step_sw[2];  // ... per-step switch counts (alternating)
+    unsigned long long nD_sum;      // ... |D| summed over its steps
+    unsigned long long nE_sum;      // ... |E| summed over its steps
     // ---- not reset per valuation ----
     unsigned long long bad_index;   // ULLONG_MAX = none, else min invalid ABI index
     unsigned long long nhard;       // vertices deferred to the hard (full-compare) pass
@@ -92,6 +97,7 @@ struct DevGame {
     uint32_t *dmark;    // epoch marks: v in D
     uint32_t *emark;    // epoch marks: v in E
     int32_t *Dl;        // D list
+    uint2 *Dr;          // reverse-CSR range [rrp[v], rrp[v+1]) of each D-list entry
     int32_t *El;        // E list
     uint32_t epoch;     // current incremental epoch
     uint32_t *cmark;    // epoch marks: v in C
@@ -121,6 +127,9 @@ struct DevGame {
     int64_t sh_even_lo, sh_even_hi, sh_odd_lo, sh_odd_hi;
     int32_t sharded;
     int32_t trace_ts;   // PGSI_TRACE=2: record phase timestamps in ctl->ts
+    int32_t inc_max_steps;  // inner iterations one k_inc_iter launch may run (>= 1)
+    int32_t inc_grid_cap;   // cooperative grid cap of k_inc_iter
+    int64_t inc_s_div;      // incremental step only while |S| * inc_s_div <= n'
 };
 
 struct LaunchCfg {

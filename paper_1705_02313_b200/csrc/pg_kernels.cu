@@ -1038,10 +1038,10 @@ __device__ __forceinline__ void warp_append8(const int32_t (&u)[8], const bool (
         if (ok[j]) list[pos++] = u[j];
 }
 
-// Expand the reverse edges [rb, re) of item f (-1 = none) 8 at a time with the
-// loads and atomics of a batch issued together. MODE 0: functional children of f
-// (succ(u) == f) newly marked in mark (D closure); MODE 1: Odd predecessors
-// (u >= lo_owner) newly marked (E); MODE 2: Even predecessors (u < n_even).
+// Expand the reverse edges [rb, re) 8 at a time with the loads and atomics of a
+// batch issued together. MODE 1: Odd predecessors (u >= n_even) newly marked in
+// mark (E); MODE 2: Even predecessors (u < n_even). (The D closure has its own
+// expansion, expand_closure.)
 template <int MODE>
 __device__ __forceinline__ void expand_rev(const DevGame &g, int32_t f, uint32_t rb, uint32_t re, uint32_t *mark,
                                            uint32_t ep, int32_t *out, unsigned long long *cnt) {
@@ -1051,10 +1051,8 @@ __device__ __forceinline__ void expand_rev(const DevGame &g, int32_t f, uint32_t
         bool ok[8];
 #pragma unroll
         for (int j = 0; j < 8; j++) u[j] = (rb + k0 + j < re) ? __ldg(g.rcol + rb + k0 + j) : -1;
-        if constexpr (MODE == 0) {
-#pragma unroll
-            for (int j = 0; j < 8; j++) ok[j] = u[j] >= 0 && __ldcg(g.succ + u[j]) == f;
-        } else if constexpr (MODE == 1) {
+        static_assert(MODE == 1 || MODE == 2, "expand_rev: MODE 1 (Odd) or 2 (Even)");
+        if constexpr (MODE == 1) {
 #pragma unroll
             for (int j = 0; j < 8; j++) ok[j] = u[j] >= 0 && u[j] >= g.n_even;
         } else {
@@ -1064,6 +1062,62 @@ __device__ __forceinline__ void expand_rev(const DevGame &g, int32_t f, uint32_t
 #pragma unroll
         for (int j = 0; j < 8; j++) ok[j] = ok[j] && atomicExch(mark + u[j], ep) != ep;
         warp_append8(u, ok, out, cnt);
+    }
+}
+
+// Dirty-closure expansion of frontier vertex f (-1 = none) with reverse range
+// [rb, re): the functional children u of f (succ(u) == f) join D. A vertex has one
+// successor, so it is discovered by at most one frontier vertex; only members of
+// S (marked before the first level) can be met twice, so a plain mark load
+// replaces the atomic exchange. The child's own reverse range is loaded in the
+// same step as its succ and stored beside it (the next level starts at rcol).
+__device__ __forceinline__ void expand_closure(const DevGame &g, int32_t f, uint32_t rb, uint32_t re,
+                                               uint32_t ep, int32_t *outv, uint2 *outr,
+                                               unsigned long long *cnt) {
+    const int lane = threadIdx.x & 31;
+    const int maxd = (int)__reduce_max_sync(FULL, re - rb);
+    for (int k0 = 0; k0 < maxd; k0 += 8) {
+        int32_t u[8];
+        bool ok[8];
+        uint32_t ub[8], ue[8];
+#pragma unroll
+        for (int j = 0; j < 8; j++) u[j] = (rb + k0 + j < re) ? __ldg(g.rcol + rb + k0 + j) : -1;
+        int32_t su[8];
+        uint32_t mk[8];
+        // all loads of the batch issued together (no control dependence between them)
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            const int32_t x = u[j] >= 0 ? u[j] : 0;
+            su[j] = __ldcg(g.succ + x);
+            mk[j] = __ldcg(g.dmark + x);
+            ub[j] = __ldg(g.rrp + x);
+            ue[j] = __ldg(g.rrp + x + 1);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; j++) ok[j] = u[j] >= 0 && su[j] == f && mk[j] != ep;
+        int c = 0;
+#pragma unroll
+        for (int j = 0; j < 8; j++) c += ok[j];
+        int incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int t = __shfl_up_sync(FULL, incl, o);
+            if (lane >= o) incl += t;
+        }
+        const int total = __shfl_sync(FULL, incl, 31);
+        if (total == 0) continue;
+        unsigned long long base = 0;
+        if (lane == 31) base = atomicAdd(cnt, (unsigned long long)total);
+        base = __shfl_sync(FULL, base, 31);
+        unsigned long long pos = base + (unsigned long long)(incl - c);
+#pragma unroll
+        for (int j = 0; j < 8; j++)
+            if (ok[j]) {
+                g.dmark[u[j]] = ep;
+                outv[pos] = u[j];
+                outr[pos] = make_uint2(ub[j], ue[j]);
+                pos++;
+            }
     }
 }
 
@@ -1078,7 +1132,6 @@ __device__ __forceinline__ void trace_ts(const DevGame &g, int k) {
 __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
     __shared__ uint8_t hsm[kThreads][36];
     __shared__ uint32_t osm[kThreads][9];
-    const uint32_t ep = g.epoch;
     const int64_t N = g.n_int;
     const uint32_t SINK = (uint32_t)N;
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -1087,6 +1140,12 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
     const int64_t wbase = tid - lane;
     Ctl *ctl = g.ctl;
 
+    // Consecutive inner iterations run in this one launch (Algorithm 1's inner
+    // loop, kept on the device) while each stays incremental;
+    // step t uses epoch g.epoch + t for its D / E marks (the host reserves them).
+    for (int step = 0;; step++) {
+    const uint32_t ep = g.epoch + (uint32_t)step;
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->steps_done = (unsigned long long)step;
     trace_ts(g, 0);
     // ---- 1. dirty closure
     const int64_t ns = (int64_t)__ldcg(&ctl->nswl);
@@ -1094,6 +1153,7 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
         const int32_t v = __ldcg(g.swl + i).x;
         g.dmark[v] = ep;
         g.Dl[i] = v;
+        g.Dr[i] = make_uint2(__ldg(g.rrp + v), __ldg(g.rrp + v + 1));
     }
     gbar(ctl);
     if (blockIdx.x == 0 && threadIdx.x == 0) { ctl->nswl = 0; ctl->nhard = 0; }  // step 5 appends anew
@@ -1106,13 +1166,12 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
         for (int64_t b0 = lo + wbase; b0 < hi; b0 += stride) {
             const int64_t i = b0 + lane;
             int32_t f = -1;
-            uint32_t rb = 0, re = 0;
+            uint2 r = make_uint2(0u, 0u);
             if (i < hi) {
                 f = __ldcg(g.Dl + i);
-                rb = __ldg(g.rrp + f);
-                re = __ldg(g.rrp + f + 1);
+                r = __ldcg(g.Dr + i);
             }
-            expand_rev<0>(g, f, rb, re, g.dmark, ep, out, cnt);
+            expand_closure(g, f, r.x, r.y, ep, out, g.Dr + hi, cnt);
         }
         gbar(ctl);
         const int64_t added = (int64_t)bcast_ld(cnt);
@@ -1217,9 +1276,9 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
         const int64_t i = b0 + lane;
         uint32_t rb = 0, re = 0;
         if (i < nd) {
-            const int32_t f = __ldcg(g.Dl + i);
-            rb = __ldg(g.rrp + f);
-            re = __ldg(g.rrp + f + 1);
+            const uint2 r = __ldcg(g.Dr + i);
+            rb = r.x;
+            re = r.y;
         }
         expand_rev<1>(g, -1, rb, re, g.emark, ep, g.El, &ctl->nE);
     }
@@ -1257,7 +1316,10 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
         g.succ[e.x] = e.y;
     }
     unsigned long long t = block_sum(nsw);
-    if (threadIdx.x == 0 && t) atomicAdd(&ctl->odd_switches, t);
+    if (threadIdx.x == 0 && t) {
+        atomicAdd(&ctl->odd_switches, t);
+        atomicAdd(&ctl->step_sw[step & 1], t);
+    }
     t = block_sum(reads);
     if (threadIdx.x == 0 && t) atomicAdd(&ctl->rows_odd, t);
     t = block_sum(fulls);
@@ -1270,6 +1332,29 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
         ctl->v1_rounds = (unsigned long long)r;
     }
     trace_ts(g, 8);
+    if (ovf) return;   // walk overflow: nothing switched; the host redoes this step in full
+
+    // ---- 8. next inner iteration on the device while it stays incremental:
+    // S = this step's switch list (nswl), applied above
+    gbar(ctl);
+    const unsigned long long sw = bcast_ld(&ctl->step_sw[step & 1]);
+    const int64_t nsn = (int64_t)bcast_ld(&ctl->nswl);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {   // every reader of these is behind a barrier
+        ctl->steps_done = (unsigned long long)step + 1;
+        ctl->last_sw = sw;
+        ctl->nD_sum += (unsigned long long)nd;
+        ctl->nE_sum += (unsigned long long)ne;
+        ctl->step_sw[(step + 1) & 1] = 0;
+        ctl->dcnt[0] = ctl->dcnt[1] = ctl->dcnt[2] = 0;
+        ctl->newfin[0] = ctl->newfin[1] = ctl->newfin[2] = 0;
+        ctl->nE = 0;
+    }
+    const int64_t need = (nsn * 16 + kThreads - 1) / kThreads;   // the grid the host would pick
+    if (sw == 0 || step + 1 >= g.inc_max_steps || nsn * g.inc_s_div > N ||
+        (need > (int64_t)gridDim.x && (int)gridDim.x < g.inc_grid_cap))
+        return;
+    gbar(ctl);   // the resets above precede the next step's appends
+    }
 }
 
 

@@ -228,8 +228,11 @@ def test_solve_device_pointers_and_caps(pg):
     np.testing.assert_array_equal(res.winner.cpu().numpy(), ora.winner)
     np.testing.assert_array_equal(res.tau.cpu().numpy(), ora.tau)
     np.testing.assert_array_equal(res.val.cpu().numpy(), ora.val)
-    # one timed valuation per inner iteration (full or incremental) + the val export
-    assert res.stats["n_v1"] + res.stats["n_inc"] + res.stats["n_bfs"] >= ora.inner_iters + 1
+    # every inner iteration is a full (timed V1) or an incremental valuation, + the val export;
+    # one incremental launch may run several inner iterations on the device
+    st = res.stats
+    assert st["n_v1"] + st["inc_valuations"] + st["n_bfs"] >= ora.inner_iters + 1
+    assert st["n_inc"] <= st["inc_valuations"] + st["inc_aborts"]
     assert res.stats["ms_v1"] > 0
     # repeated solves on the same handle are identical
     res2 = G.solve(want_val=True)
@@ -378,3 +381,21 @@ def test_bfs_abort_on_deep_game(pg):
     r = pg.Game.from_game(g, bfs=True).solve(want_val=True)
     assert r.stats["bfs_aborts"] > 0
     assert_solve_equal(r, ora, g.n, r.val.shape[1])
+
+
+def test_inc_multi_step_launches(pg, monkeypatch):
+    """Several inner iterations per incremental launch (k_inc_iter step 8, the inner
+    loop kept on the device) give the same solve as one iteration per launch
+    (PGSI_INC_STEPS=1), and actually run more than one step per launch."""
+    g = gi.random_game(200000, 16, 2, 5, 21)
+    ora = Oracle(g).solve()
+    runs = {}
+    for steps in ("1", "1000000"):
+        monkeypatch.setenv("PGSI_INC_STEPS", steps)
+        G = pg.Game.from_game(g, phase_timing=True)
+        res = G.solve(want_val=True)
+        assert_solve_equal(res, ora, g.n, G.d)
+        runs[steps] = res.stats
+    assert runs["1"]["n_inc"] >= runs["1"]["inc_valuations"]
+    assert runs["1000000"]["inc_valuations"] > 0
+    assert runs["1000000"]["n_inc"] < runs["1000000"]["inc_valuations"]
