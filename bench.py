@@ -227,7 +227,8 @@ def main():
                             "bytes_v2", "bytes_odd", "bytes_even", "bytes_inc", "n_v1", "n_v2", "n_odd",
                             "n_even", "n_inc", "gpu_launches", "inner_iters", "outer_passes",
                             "full_compares", "v1_rounds", "v2_split_valuations", "inc_valuations",
-                            "dirty_vertices", "ms_bfs", "n_bfs", "bytes_bfs", "bfs_valuations")}
+                            "dirty_vertices", "ms_bfs", "n_bfs", "bytes_bfs", "bfs_valuations",
+                            "prefix_gathers")}
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     barrier()
@@ -340,6 +341,7 @@ def main():
                        "seed": args.seed, "n_internal": G.n_internal, "m": int(game.m),
                        "inner_iters": inner, "outer_passes": outer, "solve_ms": ms / args.steps,
                        "full_compares_per_solve": int(acc["full_compares"] / args.steps),
+                       "prefix_gathers_per_solve": int(acc["prefix_gathers"] / args.steps),
                        "v1_rounds_per_solve": int(acc["v1_rounds"] / args.steps),
                        "split_valuations_per_solve": int(acc["v2_split_valuations"] / args.steps),
                        "incremental_valuations_per_solve": int(acc["inc_valuations"] / args.steps),

@@ -142,6 +142,8 @@ typedef struct {
     int64_t dist_exchanges;  /* switch-list exchanges with the other ranks (pg_dist_attach) */
     int64_t dist_bytes;      /* device bytes this rank sent through the exchange            */
     double ms_dist;          /* host wall time inside the exchange callback                 */
+    int64_t prefix_gathers;  /* 32 B prefix gathers of the switch steps after an undecided
+                                8 B switch-key compare (DESIGN.md §4 switch keys)          */
 } pg_stats;
 
 /* pg_load: validate, canonicalise and preprocess a game, copy it to the GPU.

@@ -284,14 +284,16 @@ void note_valuation(pg_game h, bool full_rows, bool inc, bool bfs = false) {
         // per dirty vertex: reverse edges scanned with the predecessors' succ (≈ 8 B × in-degree),
         // D list + reverse range w+r, succ, jl w+r, pidx, ⊤, the exit vertex's prefix and its own
         // prefix; per E vertex its list entry, mark, CSR range, successors and the prefix gathers
-        h->st.bytes_inc += nd * (8.0 * h->avg_indeg + 8.0 + 16.0 + 4.0 + 16.0 + 1.0 + 1.0 + 32.0 + 32.0) +
-                           4.0 * ne + 12.0 * ne + 4.0 * h->avg_indeg * ne + 32.0 * (double)h->h_ctl->rows_odd +
+        h->st.bytes_inc += nd * (8.0 * h->avg_indeg + 8.0 + 16.0 + 4.0 + 16.0 + 1.0 + 1.0 + 32.0 + 40.0) +
+                           4.0 * ne + 12.0 * ne + 4.0 * h->avg_indeg * ne + 8.0 * (double)h->h_ctl->rows_odd +
+                           32.0 * (double)h->h_ctl->cpx_gathers +
                            8.0 * (double)h->h_ctl->odd_switches;
         h->st.odd_switches += (int64_t)h->h_ctl->odd_switches;
         h->st.full_compares += (int64_t)h->h_ctl->full_odd;
+        h->st.prefix_gathers += (int64_t)h->h_ctl->cpx_gathers;
     } else {
         h->st.bytes_v1 += 5.0 * np_;
-        h->st.bytes_v2 += np_ + (full_rows ? R * (double)h->h_ctl->n_fin : 32.0 * np_);
+        h->st.bytes_v2 += np_ + (full_rows ? R * (double)h->h_ctl->n_fin : 40.0 * np_);   // prefix + key
         h->st.top_vertices += (int64_t)h->h_ctl->n_top;
         if ((int64_t)h->h_ctl->maxdepth > h->st.max_depth) h->st.max_depth = (int64_t)h->h_ctl->maxdepth;
         if ((int64_t)h->h_ctl->maxdepth >= h->G.K) h->st.v2_split_valuations++;
@@ -462,9 +464,11 @@ pg_status inner_loop(pg_game h, int64_t *inner, bool check) {
             const int64_t c = (int64_t)h->h_ctl->odd_switches;
             h->st.odd_switches += c;
             const double no = (double)(h->G.n_int - h->G.n_even), mo = (double)h->m_odd;
-            h->st.bytes_odd += 4.0 * (no + 1) + 4.0 * no + 4.0 * mo + 32.0 * (double)h->h_ctl->rows_odd +
+            h->st.bytes_odd += 4.0 * (no + 1) + 4.0 * no + 4.0 * mo + 8.0 * (double)h->h_ctl->rows_odd +
+                               32.0 * (double)h->h_ctl->cpx_gathers +
                                8.0 * h->G.dp * (double)h->h_ctl->full_odd + 4.0 * c;
             h->st.full_compares += (int64_t)h->h_ctl->full_odd;
+            h->st.prefix_gathers += (int64_t)h->h_ctl->cpx_gathers;
         }
         if (so.sw_last == 0) return PG_OK;
     }
@@ -475,6 +479,7 @@ pg_status inner_loop(pg_game h, int64_t *inner, bool check) {
 pg_status even_switch(pg_game h, int64_t *count) {
     CK(h, cudaMemsetAsync(&h->G.ctl->even_switches, 0, sizeof(unsigned long long), h->stream));
     CK(h, cudaMemsetAsync(&h->G.ctl->rows_even, 0, sizeof(unsigned long long), h->stream));
+    CK(h, cudaMemsetAsync(&h->G.ctl->cpx_gathers, 0, sizeof(unsigned long long), h->stream));
     CK(h, cudaMemsetAsync(&h->G.ctl->full_even, 0, sizeof(unsigned long long), h->stream));
     const bool inc = h->c_valid && !(h->flags & PG_NO_INCREMENTAL) && h->h_ctl->nC * 8 <= (uint64_t)h->G.n_int;
     {
@@ -505,9 +510,11 @@ pg_status even_switch(pg_game h, int64_t *count) {
         const double ne = inc ? (double)h->h_ctl->nE : (double)h->G.n_even;
         const double me = inc ? h->avg_indeg * ne : (double)(h->m_int - h->m_odd);
         const double cl = inc ? (double)h->h_ctl->nC * (4.0 + 8.0 * h->avg_indeg) : 0.0;
-        h->st.bytes_even += cl + 4.0 * (ne + 1) + 4.0 * ne + 4.0 * me + 32.0 * (double)h->h_ctl->rows_even +
+        h->st.bytes_even += cl + 4.0 * (ne + 1) + 4.0 * ne + 4.0 * me + 8.0 * (double)h->h_ctl->rows_even +
+                            32.0 * (double)h->h_ctl->cpx_gathers +
                             8.0 * h->G.dp * (double)h->h_ctl->full_even + 4.0 * *count;
         h->st.full_compares += (int64_t)h->h_ctl->full_even;
+        h->st.prefix_gathers += (int64_t)h->h_ctl->cpx_gathers;
         if (inc) h->st.inc_even_switches++;
     }
     // a new C starts: changes after this All_Even
@@ -726,6 +733,7 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     CKL(dalloc(h, &G.jl, N1));
     CKL(dalloc(h, &G.top, N1));
     CKL(dalloc(h, &G.cpx, N1 * 8));
+    CKL(dalloc(h, &G.key, N1));
     CKL(dalloc(h, &G.hard, N1));
     CKL(dalloc(h, &G.swl, N1));
     CKL(dalloc(h, &G.sidx, N1));
@@ -738,6 +746,7 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     if (L.d) CKL(cudaMemcpyAsync(h->d_D, L.D.data(), sizeof(int32_t) * L.d, cudaMemcpyHostToDevice, s));
     CKL(cudaMemsetAsync(G.top, 0, N1, s));
     CKL(cudaMemsetAsync(G.cpx, 0, sizeof(uint32_t) * N1 * 8, s));   // sink prefix = zero row
+    CKL(cudaMemsetAsync(G.key, 0, sizeof(uint2) * N1, s));          // sink key = zeros
     // incremental-valuation state (§V-inc)
     CKL(dalloc(h, &G.dmark, N1));
     CKL(dalloc(h, &G.emark, N1));

@@ -63,6 +63,7 @@ struct Ctl {
     unsigned long long step_sw[2];  // ... per-step switch counts (alternating)
     unsigned long long nD_sum;      // ... |D| summed over its steps
     unsigned long long nE_sum;      // ... |E| summed over its steps
+    unsigned long long cpx_gathers; // switch steps: 32 B prefix gathers after an undecided key compare
     // ---- not reset per valuation ----
     unsigned long long bad_index;   // ULLONG_MAX = none, else min invalid ABI index
     unsigned long long nhard;       // vertices deferred to the hard (full-compare) pass
@@ -91,6 +92,7 @@ struct DevGame {
     uint8_t *top;
     int32_t *val;
     uint32_t *cpx;      // compact prefixes, 8 words per vertex (+ sink row of zeros)
+    uint2 *key;         // switch keys: first two prefix words (put_cpx; sink = zeros)
     int32_t *hard;      // switch worklist of vertices with undecided prefixes
     const uint32_t *rrp;   // reverse CSR (predecessors in the game graph), device order
     const int32_t *rcol;

@@ -353,11 +353,24 @@ __device__ __forceinline__ void cpx_chunk(Cpx &p, const uint32_t (&h)[8], const 
     }
 }
 
-__device__ __forceinline__ void cpx_store(uint32_t *cpx, int64_t v, const Cpx &p, bool top) {
-    uint4 *dst = reinterpret_cast<uint4 *>(cpx + v * 8);
-    const uint32_t hdr = top ? 1u : (((uint32_t)p.np << 2) | (p.trunc ? 2u : 0u));
-    dst[0] = make_uint4(hdr, p.w[1], p.w[2], p.w[3]);
-    dst[1] = make_uint4(p.w[4], p.w[5], p.w[6], p.w[7]);
+// 8-byte switch key of a compact prefix: its first two pair words, so that most ⊑
+// decisions of the switch step gather 8 B per candidate from a table that fits in
+// L2 (n′·8 B = 107 MB at config 3) instead of 32 B from a 427 MB one. ⊤ is
+// (INT_MAX, INT_MAX) (no pair word reaches it); a word beyond a truncated prefix
+// is INT_MIN (no pair word reaches it either), meaning "unknown".
+__device__ __forceinline__ uint2 cpx_key(uint32_t h, uint32_t w1, uint32_t w2) {
+    if (h & 1u) return make_uint2(0x7fffffffu, 0x7fffffffu);
+    const uint32_t np = (h >> 2) & 7u;
+    const bool tr = (h & 2u) != 0;
+    return make_uint2((np >= 1 || !tr) ? w1 : 0x80000000u, (np >= 2 || !tr) ? w2 : 0x80000000u);
+}
+
+// Store the 32-byte compact prefix of v and its switch key.
+__device__ __forceinline__ void put_cpx(const DevGame &g, int64_t v, uint4 a, uint4 b) {
+    uint4 *dst = reinterpret_cast<uint4 *>(g.cpx + v * 8);
+    dst[0] = a;
+    dst[1] = b;
+    g.key[v] = cpx_key(a.x, a.y, a.z);
 }
 
 // V2, full-row form (outputs only: pg_valuate, val of pg_solve / pg_best_response):
@@ -465,9 +478,7 @@ __device__ __forceinline__ void cpx_merge_store(const DevGame &g, int64_t v, uin
     }
     for (int k = np; k < 7; k++) ow[1 + k] = 0;
     ow[0] = ((uint32_t)np << 2) | (trunc ? 2u : 0u);
-    uint4 *dst = reinterpret_cast<uint4 *>(g.cpx + v * 8);
-    dst[0] = make_uint4(ow[0], ow[1], ow[2], ow[3]);
-    dst[1] = make_uint4(ow[4], ow[5], ow[6], ow[7]);
+    put_cpx(g, v, make_uint4(ow[0], ow[1], ow[2], ow[3]), make_uint4(ow[4], ow[5], ow[6], ow[7]));
 }
 
 // V2, compact form (the solve loop), dp <= 32: one thread per vertex walks its
@@ -495,10 +506,8 @@ __global__ void __launch_bounds__(kThreads) k_v2_cpx(DevGame g) {
         const unsigned long long e = __ldcg(g.jl + v);
         const bool fin = (uint32_t)e == (uint32_t)N;
         g.top[v] = fin ? 0 : 1;
-        uint4 *dst = reinterpret_cast<uint4 *>(g.cpx + v * 8);
         if (!fin) {
-            dst[0] = make_uint4(1u, 0, 0, 0);
-            dst[1] = make_uint4(0, 0, 0, 0);
+            put_cpx(g, v, make_uint4(1u, 0, 0, 0), make_uint4(0, 0, 0, 0));
             continue;
         }
         const uint32_t depth = (uint32_t)(e >> 32);
@@ -546,9 +555,7 @@ __global__ void __launch_bounds__(kThreads) k_spl_cpx(DevGame g) {
             if (cap) trunc = true;
         }
         w[0] = ((uint32_t)np << 2) | (trunc ? 2u : 0u);
-        uint4 *dst = reinterpret_cast<uint4 *>(g.cpx + (int64_t)__ldcg(g.spl + i) * 8);
-        dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
-        dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+        put_cpx(g, (int64_t)__ldcg(g.spl + i), make_uint4(w[0], w[1], w[2], w[3]), make_uint4(w[4], w[5], w[6], w[7]));
     }
 }
 
@@ -628,9 +635,7 @@ __global__ void __launch_bounds__(kThreads) k_v2_cpx_multi(DevGame g, int nchunk
             }
         }
         ow[0] = fin ? (((uint32_t)np << 2) | (trunc ? 2u : 0u)) : 1u;
-        uint4 *dst = reinterpret_cast<uint4 *>(g.cpx + v * 8);
-        dst[0] = make_uint4(ow[0], ow[1], ow[2], ow[3]);
-        dst[1] = make_uint4(ow[4], ow[5], ow[6], ow[7]);
+        put_cpx(g, v, make_uint4(ow[0], ow[1], ow[2], ow[3]), make_uint4(ow[4], ow[5], ow[6], ow[7]));
     }
 }
 
@@ -867,24 +872,56 @@ __device__ __forceinline__ bool sh_owns(const DevGame &g, int64_t v) {
     return v < g.n_even ? (v >= g.sh_even_lo && v < g.sh_even_hi) : (v >= g.sh_odd_lo && v < g.sh_odd_hi);
 }
 
-// One vertex of All_Odd / All_Even. HARD = false: compact prefixes only; a vertex
-// meeting an undecided comparison is appended to the hard list and left
-// unchanged. HARD = true: the hard list, resolving ties with cmp_full.
+// ⊑ on switch keys (cpx_key): -1 / 0 / 1, or 2 when the two known words tie (or a
+// deciding word is unknown) and the full prefixes must decide. Every decision
+// equals cmp_cpx's on the same vertices: the first differing known word decides
+// both; a tie with second words 0 means both prefixes have at most one pair and
+// are untruncated, hence equal.
+__device__ __forceinline__ int cmp_key(uint2 a, uint2 b) {
+    constexpr uint32_t TOPK = 0x7fffffffu, UNK = 0x80000000u;
+    if (a.x == TOPK || b.x == TOPK) return a.x == b.x ? 0 : (a.x == TOPK ? 1 : -1);
+    if (a.x == UNK || b.x == UNK) return 2;
+    if (a.x != b.x) return (int32_t)a.x < (int32_t)b.x ? -1 : 1;
+    if (a.y == UNK || b.y == UNK) return 2;
+    if (a.y != b.y) return (int32_t)a.y < (int32_t)b.y ? -1 : 1;
+    return a.y == 0 ? 0 : 2;
+}
+
+// ⊑ of val(a), val(b) from their 32-byte prefixes (after an undecided key
+// compare); HARD: resolve an undecided prefix compare by re-walking the plays.
+template <bool HARD>
+__device__ __forceinline__ int cmp_pref(const DevGame &g, const uint4 *cpx, int32_t a, int32_t b,
+                                        unsigned long long &pref, unsigned long long &fulls) {
+    const uint4 a0 = __ldg(cpx + 2 * (int64_t)a), a1 = __ldg(cpx + 2 * (int64_t)a + 1);
+    const uint4 b0 = __ldg(cpx + 2 * (int64_t)b), b1 = __ldg(cpx + 2 * (int64_t)b + 1);
+    pref += 2;
+    const uint32_t wa[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+    const uint32_t wb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+    int r = cmp_cpx(wa, wb);
+    if (r == 2 && HARD) {
+        r = cmp_full(g, a, b);
+        fulls++;
+    }
+    return r;
+}
+
+// One vertex of All_Odd / All_Even. HARD = false: switch keys, then compact
+// prefixes; a vertex meeting an undecided comparison is appended to the hard list
+// and left unchanged. HARD = true: the hard list, resolving ties with cmp_full.
 template <bool ODD, bool HARD>
 __device__ __forceinline__ int switch_vertex(const DevGame &g, int64_t v, const uint4 *cpx,
-                                             unsigned long long &reads, unsigned long long &fulls) {
+                                             unsigned long long &reads, unsigned long long &fulls,
+                                             unsigned long long &pref) {
     constexpr int B = 4;
     const int32_t SINK = (int32_t)g.n_int;
     const int32_t cur = __ldg(g.succ + v);
     const uint32_t beg = __ldg(g.rp + v), end = __ldg(g.rp + v + 1);
     const int32_t ncand = (int32_t)(end - beg) + (ODD ? 0 : 1);
     int32_t best = -1;
-    uint32_t bw[8], cw[8];
-#pragma unroll
-    for (int j = 0; j < 8; j++) { bw[j] = 0; cw[j] = 0; }
+    uint2 bk = make_uint2(0u, 0u), ck = make_uint2(0u, 0u);
     for (int k0 = 0; k0 < ncand; k0 += B) {
         int32_t c[B];
-        uint4 x0[B], x1[B];
+        uint2 kk[B];
 #pragma unroll
         for (int k = 0; k < B; k++) {
             const int e = k0 + k;
@@ -893,45 +930,37 @@ __device__ __forceinline__ int switch_vertex(const DevGame &g, int64_t v, const 
         }
 #pragma unroll
         for (int k = 0; k < B; k++) {
+            kk[k] = make_uint2(0u, 0u);
             if (c[k] >= 0) {
-                x0[k] = __ldg(cpx + 2 * (int64_t)c[k]);
-                x1[k] = __ldg(cpx + 2 * (int64_t)c[k] + 1);
+                kk[k] = __ldg(g.key + c[k]);
                 reads += (c[k] != SINK);
-            } else {
-                x0[k] = make_uint4(0, 0, 0, 0);
-                x1[k] = x0[k];
             }
         }
 #pragma unroll
         for (int k = 0; k < B; k++) {
             if (c[k] < 0) continue;
-            const uint32_t w[8] = {x0[k].x, x0[k].y, x0[k].z, x0[k].w, x1[k].x, x1[k].y, x1[k].z, x1[k].w};
-            if (c[k] == cur) {
-#pragma unroll
-                for (int j = 0; j < 8; j++) cw[j] = w[j];
-            }
+            if (c[k] == cur) ck = kk[k];
             bool take = best < 0;
             if (!take) {
-                int r = cmp_cpx(w, bw);
+                int r = cmp_key(kk[k], bk);
                 if (r == 2) {
-                    if constexpr (!HARD) return 2;
-                    else { r = cmp_full(g, c[k], best); fulls++; }
+                    r = cmp_pref<HARD>(g, cpx, c[k], best, pref, fulls);
+                    if (r == 2) return 2;   // (!HARD only)
                 }
                 take = ODD ? r < 0 : r > 0;
             }
             if (take) {
                 best = c[k];
-#pragma unroll
-                for (int j = 0; j < 8; j++) bw[j] = w[j];
+                bk = kk[k];
             }
         }
     }
     int r = 0;
-    if (best != cur) {
-        r = cmp_cpx(bw, cw);
+    if (best != cur) {   // cur is a candidate (an edge, or the sink for Even), so ck is its key
+        r = cmp_key(bk, ck);
         if (r == 2) {
-            if constexpr (!HARD) return 2;
-            else { r = cmp_full(g, best, cur); fulls++; }
+            r = cmp_pref<HARD>(g, cpx, best, cur, pref, fulls);
+            if (r == 2) return 2;
         }
     }
     if (ODD ? r < 0 : r > 0) {
@@ -962,12 +991,12 @@ __global__ void __launch_bounds__(kThreads) k_switch(DevGame g, const int32_t *v
     const int64_t hi = HARD ? (int64_t)__ldcg(&g.ctl->nhard)
                             : (lst ? (int64_t)__ldcg(&g.ctl->nE) : (ODD ? g.sh_odd_hi : g.sh_even_hi));
     const uint4 *cpx = reinterpret_cast<const uint4 *>(g.cpx);
-    unsigned long long nsw = 0, reads = 0, fulls = 0;
+    unsigned long long nsw = 0, reads = 0, fulls = 0, pref = 0;
     for (int64_t i = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < hi;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t v = HARD ? (int64_t)__ldcg(g.hard + i) : (lst ? (int64_t)__ldcg(vlist + i) : i);
         if (lst && g.sharded && !sh_owns(g, v)) continue;   // another rank's vertex
-        const int r = switch_vertex<ODD, HARD>(g, v, cpx, reads, fulls);
+        const int r = switch_vertex<ODD, HARD>(g, v, cpx, reads, fulls, pref);
         if (r == 1) nsw++;
         if constexpr (!HARD) {
             if (r == 2) g.hard[atomicAdd(&g.ctl->nhard, 1ull)] = (int32_t)v;
@@ -977,6 +1006,8 @@ __global__ void __launch_bounds__(kThreads) k_switch(DevGame g, const int32_t *v
     if (threadIdx.x == 0 && t) atomicAdd(ODD ? &g.ctl->odd_switches : &g.ctl->even_switches, t);
     t = block_sum(reads);
     if (threadIdx.x == 0 && t) atomicAdd(ODD ? &g.ctl->rows_odd : &g.ctl->rows_even, t);
+    t = block_sum(pref);
+    if (threadIdx.x == 0 && t) atomicAdd(&g.ctl->cpx_gathers, t);
     if constexpr (HARD) {
         t = block_sum(fulls);
         if (threadIdx.x == 0 && t) atomicAdd(ODD ? &g.ctl->full_odd : &g.ctl->full_even, t);
@@ -1251,9 +1282,7 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
         const bool fin = (uint32_t)e == SINK;
         g.top[v] = fin ? 0 : 1;
         if (!fin) {
-            uint4 *dst = reinterpret_cast<uint4 *>(g.cpx + (int64_t)v * 8);
-            dst[0] = make_uint4(1u, 0, 0, 0);
-            dst[1] = make_uint4(0, 0, 0, 0);
+            put_cpx(g, v, make_uint4(1u, 0, 0, 0), make_uint4(0, 0, 0, 0));
             continue;
         }
         uint32_t mask = 0, steps = 0;
@@ -1289,12 +1318,12 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
 
     // ---- 5-7. All_Odd over E: prefix pass, hard pass, apply
     const uint4 *cpx = reinterpret_cast<const uint4 *>(g.cpx);
-    unsigned long long nsw = 0, reads = 0, fulls = 0;
+    unsigned long long nsw = 0, reads = 0, fulls = 0, pref = 0;
     if (!ovf) {
         for (int64_t i = tid; i < ne; i += stride) {
             const int64_t v = __ldcg(g.El + i);
             if (g.sharded && !sh_owns(g, v)) continue;   // another rank's vertex
-            const int rr = switch_vertex<true, false>(g, v, cpx, reads, fulls);
+            const int rr = switch_vertex<true, false>(g, v, cpx, reads, fulls, pref);
             if (rr == 1) nsw++;
             else if (rr == 2) g.hard[atomicAdd(&ctl->nhard, 1ull)] = (int32_t)v;
         }
@@ -1305,7 +1334,7 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
         const int64_t nh = (int64_t)bcast_ld(&ctl->nhard);
         for (int64_t i = tid; i < nh; i += stride) {
             const int64_t v = __ldcg(g.hard + i);
-            if (switch_vertex<true, true>(g, v, cpx, reads, fulls) == 1) nsw++;
+            if (switch_vertex<true, true>(g, v, cpx, reads, fulls, pref) == 1) nsw++;
         }
     }
     gbar(ctl);
@@ -1324,6 +1353,8 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
     if (threadIdx.x == 0 && t) atomicAdd(&ctl->rows_odd, t);
     t = block_sum(fulls);
     if (threadIdx.x == 0 && t) atomicAdd(&ctl->full_odd, t);
+    t = block_sum(pref);
+    if (threadIdx.x == 0 && t) atomicAdd(&ctl->cpx_gathers, t);
     t = block_sum(wsteps);
     if (threadIdx.x == 0 && t) atomicAdd(&ctl->walk_steps, t);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -1484,8 +1515,7 @@ __global__ void __launch_bounds__(kThreads) k_val_bfs(DevGame g) {
             const int32_t v = __ldcg(g.Dl + i);
             const int p = __ldg(g.pidx + v);
             const int32_t en = (int32_t)(((uint32_t)p << 23) + 1u);
-            cpx4[2 * (int64_t)v] = make_uint4(1u << 2, (uint32_t)(g.oddp[p] ? -en : en), 0u, 0u);
-            cpx4[2 * (int64_t)v + 1] = make_uint4(0u, 0u, 0u, 0u);
+            put_cpx(g, v, make_uint4(1u << 2, (uint32_t)(g.oddp[p] ? -en : en), 0u, 0u), make_uint4(0u, 0u, 0u, 0u));
             g.jl[v] = pack_jl(SINK, 1u);
             g.top[v] = 0;
         }
@@ -1529,8 +1559,7 @@ __global__ void __launch_bounds__(kThreads) k_val_bfs(DevGame g) {
                     for (int q = 0; q < 8; q++) w[q] = pw[q];
                     const int p = __ldg(g.pidx + u[j]);
                     cpx_insert(w, p, g.oddp[p] != 0, maxp);
-                    cpx4[2 * (int64_t)u[j]] = make_uint4(w[0], w[1], w[2], w[3]);
-                    cpx4[2 * (int64_t)u[j] + 1] = make_uint4(w[4], w[5], w[6], w[7]);
+                    put_cpx(g, u[j], make_uint4(w[0], w[1], w[2], w[3]), make_uint4(w[4], w[5], w[6], w[7]));
                     g.jl[u[j]] = pack_jl(SINK, (uint32_t)(lev + 1));
                     g.top[u[j]] = 0;
                 }
@@ -1547,8 +1576,7 @@ __global__ void __launch_bounds__(kThreads) k_val_bfs(DevGame g) {
     // vertices never reached: ⊤ (their jl word keeps jumping along the cycle)
     for (int64_t v = tid; v < N; v += stride) {
         if (!g.top[v]) continue;
-        cpx4[2 * v] = make_uint4(1u, 0u, 0u, 0u);
-        cpx4[2 * v + 1] = make_uint4(0u, 0u, 0u, 0u);
+        put_cpx(g, v, make_uint4(1u, 0u, 0u, 0u), make_uint4(0u, 0u, 0u, 0u));
         g.jl[v] = pack_jl((uint32_t)__ldg(g.succ + v), 1u);
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {

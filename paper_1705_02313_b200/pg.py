@@ -61,7 +61,8 @@ class Stats(C.Structure):
         ("dirty_vertices", C.c_int64),
         ("ms_inc", C.c_double),
         ("n_inc", C.c_int64), ("bytes_inc", C.c_double),
-        ("dist_exchanges", C.c_int64), ("dist_bytes", C.c_int64), ("ms_dist", C.c_double)]
+        ("dist_exchanges", C.c_int64), ("dist_bytes", C.c_int64), ("ms_dist", C.c_double),
+        ("prefix_gathers", C.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
