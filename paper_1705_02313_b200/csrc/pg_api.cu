@@ -53,7 +53,7 @@ struct pg_game_s {
     uint32_t epoch = 0;
     bool trace = false;               // PGSI_TRACE=1 (debug)
     bool c_valid = false;             // C covers every change since the last All_Even
-    int64_t inc_s_div = 64;           // incremental step when |S| * inc_s_div <= n'
+    int64_t inc_s_div = 16;           // incremental step when |S| * inc_s_div <= n'
     int64_t inc_max_steps = 1 << 20;  // inner iterations per incremental launch (PGSI_INC_STEPS)
     int64_t last_maxdepth = 0;        // deepest play of the last full valuation
     uint32_t cepoch = 0;
@@ -762,10 +762,10 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     G.cepoch = 1;
     h->cepoch = 1;
     // incremental-step thresholds (tuning knobs; results never depend on them)
-    G.inc_max_levels = getenv("PGSI_INC_MAX_LEVELS") ? atoi(getenv("PGSI_INC_MAX_LEVELS")) : 48;
+    G.inc_max_levels = getenv("PGSI_INC_MAX_LEVELS") ? atoi(getenv("PGSI_INC_MAX_LEVELS")) : 256;
     G.bfs_max_levels = getenv("PGSI_BFS_MAX_LEVELS") ? atoi(getenv("PGSI_BFS_MAX_LEVELS")) : 160;
     G.inc_max_dirty = std::max<int64_t>(4096, L.n_int / (getenv("PGSI_INC_DIRTY_DIV") ? atoi(getenv("PGSI_INC_DIRTY_DIV")) : 8));
-    h->inc_s_div = getenv("PGSI_INC_S_DIV") ? atoi(getenv("PGSI_INC_S_DIV")) : 64;
+    h->inc_s_div = getenv("PGSI_INC_S_DIV") ? atoi(getenv("PGSI_INC_S_DIV")) : 16;
     h->inc_max_steps = getenv("PGSI_INC_STEPS") ? std::max(1, atoi(getenv("PGSI_INC_STEPS"))) : (1 << 20);
     G.inc_s_div = h->inc_s_div;
     G.inc_grid_cap = h->lc.coop_inc;
