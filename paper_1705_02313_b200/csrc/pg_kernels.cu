@@ -1218,21 +1218,21 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
     }
     const int64_t nd = hi;
     trace_ts(g, 1);
-    // C ∪= D (every vertex whose valuation may have changed since the last All_Even)
+    trace_ts(g, 2);
+    // ---- 2. V1 on D (init), with C ∪= D (every vertex whose valuation may have
+    // changed since the last All_Even). A vertex occurs once in D, so its C mark
+    // is a plain load and store.
+    unsigned long long *jl = g.jl;
     for (int64_t b0 = wbase; b0 < nd; b0 += stride) {
         const int64_t i = b0 + lane;
         int32_t v = -1;
-        if (i < nd) v = __ldcg(g.Dl + i);
-        const bool addc = v >= 0 && atomicExch(g.cmark + v, g.cepoch) != g.cepoch;
+        if (i < nd) {
+            v = __ldcg(g.Dl + i);
+            jl[v] = pack_jl((uint32_t)__ldcg(g.succ + v), 1u);
+        }
+        const bool addc = v >= 0 && __ldcg(g.cmark + v) != g.cepoch;
+        if (addc) g.cmark[v] = g.cepoch;
         warp_append(addc, v, g.Cl, &ctl->nC);
-    }
-
-    // ---- 2. V1 on D
-    trace_ts(g, 2);
-    unsigned long long *jl = g.jl;
-    for (int64_t i = tid; i < nd; i += stride) {
-        const int32_t v = __ldcg(g.Dl + i);
-        jl[v] = pack_jl((uint32_t)__ldcg(g.succ + v), 1u);
     }
     gbar(ctl);
     int r = 0;
