@@ -769,6 +769,7 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     h->inc_max_steps = getenv("PGSI_INC_STEPS") ? std::max(1, atoi(getenv("PGSI_INC_STEPS"))) : (1 << 20);
     G.inc_s_div = h->inc_s_div;
     G.inc_grid_cap = h->lc.coop_inc;
+    G.inc_grid_mul = getenv("PGSI_INC_GRID_MUL") ? atoi(getenv("PGSI_INC_GRID_MUL")) : 16;
     G.inc_max_steps = 1;
     // children CSR scratch of the BFS valuation (§V-bfs)
     CKL(dalloc(h, &G.ccnt, N1));

@@ -131,6 +131,7 @@ struct DevGame {
     int32_t trace_ts;   // PGSI_TRACE=2: record phase timestamps in ctl->ts
     int32_t inc_max_steps;  // inner iterations one k_inc_iter launch may run (>= 1)
     int32_t inc_grid_cap;   // cooperative grid cap of k_inc_iter
+    int32_t inc_grid_mul;   // k_inc_iter grid = |S| * inc_grid_mul threads (capped)
     int64_t inc_s_div;      // incremental step only while |S| * inc_s_div <= n'
 };
 

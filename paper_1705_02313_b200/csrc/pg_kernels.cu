@@ -1380,7 +1380,7 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
         ctl->newfin[0] = ctl->newfin[1] = ctl->newfin[2] = 0;
         ctl->nE = 0;
     }
-    const int64_t need = (nsn * 16 + kThreads - 1) / kThreads;   // the grid the host would pick
+    const int64_t need = (nsn * g.inc_grid_mul + kThreads - 1) / kThreads;   // the grid the host would pick
     if (sw == 0 || step + 1 >= g.inc_max_steps || nsn * g.inc_s_div > N ||
         (need > (int64_t)gridDim.x && (int)gridDim.x < g.inc_grid_cap))
         return;
@@ -1810,7 +1810,8 @@ cudaError_t launch_even_inc(const DevGame &g, cudaStream_t s) {
 }
 
 cudaError_t launch_inc_iter(const DevGame &g, const LaunchCfg &lc, cudaStream_t s, int64_t nS) {
-    int64_t grid = (nS * 16 + kThreads - 1) / kThreads;
+    static const int64_t mul = getenv("PGSI_INC_GRID_MUL") ? atoi(getenv("PGSI_INC_GRID_MUL")) : 16;
+    int64_t grid = (nS * mul + kThreads - 1) / kThreads;
     grid = std::max<int64_t>(1, std::min<int64_t>(grid, lc.coop_inc));
     DevGame gg = g;
     void *args[] = {&gg};
