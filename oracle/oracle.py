@@ -61,6 +61,11 @@ def _load():
         L.oracle_solve.argtypes = [C.c_void_p, C.c_int64, C.c_int64, P, P, P, P, P, P, P, P,
                                    P, C.c_int64, P, C.c_int64]
         L.oracle_solve.restype = C.c_int
+        L.oracle_solve_mode.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_int64, P, P, P, P, P, P,
+                                        P, P, P, C.c_int64, P, C.c_int64]
+        L.oracle_solve_mode.restype = C.c_int
+        L.oracle_best_response_bf.argtypes = [C.c_void_p, P, P, P, P, P]
+        L.oracle_best_response_bf.restype = C.c_int
         L.oracle_switch_step.argtypes = [C.c_void_p, P, C.c_int, P, P]
         L.oracle_switch_step.restype = C.c_int
         _lib = L
@@ -149,7 +154,25 @@ class Oracle:
                                                   _p(top), _p(inner)))
         return tau, val, top, int(inner[0])
 
-    def solve(self, max_inner: int = 0, max_outer: int = 0, trace_cap: int = 1 << 16) -> SolveResult:
+    MODES = {"si": 0, "si_reset": 1, "bf": 2}
+
+    def best_response_bf(self, sigma):
+        """Bellman-Ford best response: (τ, val, top, rounds)."""
+        N, d = self.n_internal, self.d
+        s = np.ascontiguousarray(sigma, np.int32)
+        tau = np.zeros(N, np.int32)
+        val = np.zeros((N, d), np.int32)
+        top = np.zeros(N, np.uint8)
+        rounds = np.zeros(1, np.int64)
+        self._check(_load().oracle_best_response_bf(self._h, _p(s), _p(tau), _p(val), _p(top),
+                                                     _p(rounds)))
+        return tau, val, top, int(rounds[0])
+
+    def solve(self, max_inner: int = 0, max_outer: int = 0, trace_cap: int = 1 << 16,
+              mode: str = "si") -> SolveResult:
+        """Algorithm 1; mode "si" (warm-started τ), "si_reset" (τ := τ_init before every
+        best response) or "bf" (Bellman-Ford best responses; inner_iters
+        counts relaxation rounds)."""
         n, N, d = self.n, self.n_internal, self.d
         winner = np.zeros(n, np.uint8)
         sigma = np.zeros(n, np.int32)
@@ -161,7 +184,8 @@ class Oracle:
         stats = np.zeros(8, np.int64)
         ot = np.zeros(trace_cap, np.int64)
         et = np.zeros(trace_cap, np.int64)
-        self._check(_load().oracle_solve(self._h, max_inner, max_outer, _p(winner), _p(sigma),
+        self._check(_load().oracle_solve_mode(self._h, self.MODES[mode], max_inner, max_outer,
+                                              _p(winner), _p(sigma),
                                          _p(tau), _p(val), _p(succ_int), _p(val_int), _p(top_int),
                                          _p(stats), _p(ot), trace_cap, _p(et), trace_cap))
         inner, outer = int(stats[0]), int(stats[1])

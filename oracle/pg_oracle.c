@@ -19,6 +19,10 @@
  *   - switchable edges / greedy all-switches ....... §3
  *   - Algorithm 1 (inner + outer loop) ............. §4
  *   - winning sets from ⊤ ........................... §3
+ *   - SI-Reset arm (τ reset to τ_init before every
+ *     best response) ................................ §6
+ *   - Bellman-Ford best-response arm (synchronous
+ *     relaxation rounds from ⊤) ..................... §4; Table 2
  * Readings of silent/ambiguous passages are the numbered ones of SURVEY.md §8(c)
  * (restated in DESIGN.md "Readings"): tie-break = first in canonical adjacency
  * order with the sink last (3), τ_init = first successor (4), strict switches
@@ -411,6 +415,108 @@ static int og_inner(const og_game *g, int32_t *succ, og_vals *V, int64_t *inner,
     }
 }
 
+/* ⊑ on two rows given directly (counts, ⊤ flag): -1 / 0 / +1 as og_compare. */
+static int og_compare_rows(const og_game *g, const int32_t *ra, int ta, const int32_t *rb, int tb) {
+    if (ta && tb) return 0;
+    if (ta) return 1;
+    if (tb) return -1;
+    for (int32_t p = g->d - 1; p >= 0; p--) {
+        if (ra[p] == rb[p]) continue;
+        if (!g->odd_pri[p]) return ra[p] < rb[p] ? -1 : 1;
+        return ra[p] > rb[p] ? -1 : 1;
+    }
+    return 0;
+}
+
+/*
+ * Bellman-Ford best response ("find a shortest-path from each
+ * vertex to the sink, where path lengths are compared using the ⊑ ordering ...
+ * odd priorities correspond to negative edge weights"; the comparison arm of
+ * Table 2). val^σ is the fixpoint of synchronous rounds
+ *     new(v) = e_pri(v) + val(σ(v))                       v ∈ V_Even
+ *     new(v) = e_pri(v) + min_⊑ { val(u) : u ∈ adj(v) }   v ∈ V_Odd
+ * from val ≡ ⊤ with val(s) = 0 and ⊤ + e = ⊤ (reading 19). A round reads only the
+ * previous round's values. Every round computed is one iteration, the last being
+ * the first round that changes nothing. Without convergence within n'+1 rounds
+ * an Odd-reachable odd cycle exists (a negative cycle; σ inadmissible). At the
+ * fixpoint τ(v) := the first u ∈ adj(v) with ⊑-minimal val(u) (reading 3).
+ * succ holds σ on Even vertices on entry and σ ∪ τ on exit; V receives val^σ.
+ */
+static int og_bellman_ford(const og_game *g, int32_t *succ, og_vals *V, int64_t *iters, int64_t max_inner) {
+    int64_t N = g->n_int;
+    int32_t d = g->d;
+    size_t rowsz = (size_t)(d ? d : 1);
+    int32_t *cur = calloc((size_t)N * rowsz + 1, sizeof(int32_t));
+    int32_t *nxt = calloc((size_t)N * rowsz + 1, sizeof(int32_t));
+    uint8_t *tcur = malloc((size_t)N + 1), *tnxt = malloc((size_t)N + 1);
+    int32_t *zero = calloc(rowsz, sizeof(int32_t));
+    memset(tcur, 1, (size_t)N + 1);
+    int rc = OR_OK;
+    for (int64_t round = 0;; round++) {
+        if (round > N + 1) { set_err("Bellman-Ford did not converge: odd cycle (strategy not admissible)"); rc = OR_EINADMISSIBLE; break; }
+        if (max_inner > 0 && *iters >= max_inner) { set_err("inner iteration cap"); rc = OR_EITERCAP; break; }
+        int64_t changed = 0;
+        for (int64_t v = 0; v < N; v++) {
+            const int32_t *best = NULL;
+            int btop = 1;
+            if (g->owner[v] == 0) {
+                int32_t u = succ[v];
+                if (u == SINK) { best = zero; btop = 0; }
+                else { best = cur + (size_t)u * rowsz; btop = tcur[u]; }
+            } else {
+                for (int64_t e = g->adj_ptr[v]; e < g->adj_ptr[v + 1]; e++) {
+                    int32_t u = g->adj[e];
+                    if (e == g->adj_ptr[v] || og_compare_rows(g, cur + (size_t)u * rowsz, tcur[u], best, btop) < 0) {
+                        best = cur + (size_t)u * rowsz;
+                        btop = tcur[u];
+                    }
+                }
+            }
+            int32_t *row = nxt + (size_t)v * rowsz;
+            tnxt[v] = (uint8_t)btop;
+            if (btop) {
+                memset(row, 0, sizeof(int32_t) * rowsz);
+            } else {
+                memcpy(row, best, sizeof(int32_t) * rowsz);
+                row[g->pidx[v]] += 1;                                   /* + e_pri(v) */
+            }
+            if (tnxt[v] != tcur[v] || (!btop && memcmp(row, cur + (size_t)v * rowsz, sizeof(int32_t) * rowsz)))
+                changed++;
+        }
+        int32_t *t = cur; cur = nxt; nxt = t;
+        uint8_t *tt = tcur; tcur = tnxt; tnxt = tt;
+        (*iters)++;
+        if (changed == 0) break;
+    }
+    if (rc == OR_OK) {
+        for (int64_t v = 0; v < N; v++) {
+            if (g->owner[v] != 1) continue;
+            int32_t b = g->adj[g->adj_ptr[v]];
+            for (int64_t e = g->adj_ptr[v] + 1; e < g->adj_ptr[v + 1]; e++) {
+                int32_t u = g->adj[e];
+                if (og_compare_rows(g, cur + (size_t)u * rowsz, tcur[u], cur + (size_t)b * rowsz, tcur[b]) < 0) b = u;
+            }
+            succ[v] = b;
+        }
+        /* V := the fixpoint. The path walk of the profile (σ, τ) reports an odd
+         * cycle that τ would close from ⊤ vertices (reading 19). */
+        for (int64_t v = 0; v < N; v++) {
+            V->top[v] = tcur[v];
+            V->cycdom[v] = -1;
+            memcpy(V->val + (size_t)v * d, cur + (size_t)v * rowsz, sizeof(int32_t) * (size_t)d);
+        }
+        og_vals W;
+        if (og_alloc_vals(g, &W)) { rc = OR_ENOMEM; }
+        else {
+            if (og_valuate(g, succ, &W)) { set_err("odd cycle: strategy not admissible"); rc = OR_EINADMISSIBLE; }
+            for (int64_t v = 0; v < N; v++) V->cycdom[v] = W.cycdom[v];
+            og_free_vals(&W);
+        }
+    }
+    free(cur); free(nxt); free(tcur); free(tnxt); free(zero);
+    return rc;
+}
+
 int oracle_best_response(const og_game *g, const int32_t *sigma, const int32_t *tau0,
                          int32_t *tau_out, int32_t *val, uint8_t *top, int64_t *inner_iters) {
     int32_t *succ = malloc(sizeof(int32_t) * ((size_t)g->n_int + 1));
@@ -443,10 +549,13 @@ int oracle_best_response(const og_game *g, const int32_t *sigma, const int32_t *
  * Optional internal outputs (n_internal entries) sigma_int/tau_int/val_int/top_int.
  * odd_trace / even_trace (optional): switch counts per inner iteration / outer pass.
  */
-int oracle_solve(const og_game *g, int64_t max_inner, int64_t max_outer,
-                 uint8_t *winner, int32_t *sigma, int32_t *tau, int32_t *val,
-                 int32_t *succ_int, int32_t *val_int, uint8_t *top_int, int64_t *stats,
-                 int64_t *odd_trace, int64_t odd_cap, int64_t *even_trace, int64_t even_cap) {
+#define OR_MODE_SI 0        /* Algorithm 1: τ warm-started from the previous best response */
+#define OR_MODE_SI_RESET 1  /* SI-Reset: τ := τ_init before every best response */
+#define OR_MODE_BF 2        /* best responses by Bellman-Ford; inner = rounds */
+int oracle_solve_mode(const og_game *g, int mode, int64_t max_inner, int64_t max_outer,
+                      uint8_t *winner, int32_t *sigma, int32_t *tau, int32_t *val,
+                      int32_t *succ_int, int32_t *val_int, uint8_t *top_int, int64_t *stats,
+                      int64_t *odd_trace, int64_t odd_cap, int64_t *even_trace, int64_t even_cap) {
     int64_t N = g->n_int;
     int32_t *succ = malloc(sizeof(int32_t) * ((size_t)N + 1));
     /* σ_init(v) = s for Even; τ arbitrary = first successor (reading 4) */
@@ -457,7 +566,10 @@ int oracle_solve(const og_game *g, int64_t max_inner, int64_t max_outer,
     int rc = OR_OK;
     for (;;) {                                            /* repeat (outer) */
         if (max_outer > 0 && outer >= max_outer) { set_err("outer pass cap"); rc = OR_EITERCAP; break; }
-        rc = og_inner(g, succ, &V, &inner, max_inner, odd_trace, odd_cap, &otl);
+        if (mode == OR_MODE_SI_RESET && outer > 0)       /* SI-Reset: τ := τ_init */
+            for (int64_t v = 0; v < N; v++) if (g->owner[v] == 1) succ[v] = g->adj[g->adj_ptr[v]];
+        if (mode == OR_MODE_BF) rc = og_bellman_ford(g, succ, &V, &inner, max_inner);
+        else rc = og_inner(g, succ, &V, &inner, max_inner, odd_trace, odd_cap, &otl);
         if (rc) break;
         outer++;
         int64_t c = og_even_switch(g, &V, succ);          /* σ := σ[All_Even(σ)] */
@@ -484,6 +596,34 @@ int oracle_solve(const og_game *g, int64_t max_inner, int64_t max_outer,
         if (val_int) memcpy(val_int, V.val, sizeof(int32_t) * (size_t)N * (size_t)g->d);
         if (top_int) memcpy(top_int, V.top, (size_t)N);
     }
+    og_free_vals(&V);
+    free(succ);
+    return rc;
+}
+
+int oracle_solve(const og_game *g, int64_t max_inner, int64_t max_outer,
+                 uint8_t *winner, int32_t *sigma, int32_t *tau, int32_t *val,
+                 int32_t *succ_int, int32_t *val_int, uint8_t *top_int, int64_t *stats,
+                 int64_t *odd_trace, int64_t odd_cap, int64_t *even_trace, int64_t even_cap) {
+    return oracle_solve_mode(g, OR_MODE_SI, max_inner, max_outer, winner, sigma, tau, val, succ_int,
+                             val_int, top_int, stats, odd_trace, odd_cap, even_trace, even_cap);
+}
+
+/* Bellman-Ford best response against σ (Even entries of sigma).
+ * tau_out: τ = first ⊑-minimal successor at the fixpoint; inner_iters = rounds. */
+int oracle_best_response_bf(const og_game *g, const int32_t *sigma, int32_t *tau_out, int32_t *val,
+                            uint8_t *top, int64_t *inner_iters) {
+    int32_t *succ = malloc(sizeof(int32_t) * ((size_t)g->n_int + 1));
+    for (int64_t v = 0; v < g->n_int; v++) succ[v] = g->owner[v] == 0 ? sigma[v] : g->adj[g->adj_ptr[v]];
+    int rc = og_check_strategy(g, succ, 1);
+    if (rc) { free(succ); return rc; }
+    og_vals V;
+    og_alloc_vals(g, &V);
+    int64_t rounds = 0;
+    rc = og_bellman_ford(g, succ, &V, &rounds, 0);
+    if (tau_out) for (int64_t v = 0; v < g->n_int; v++) tau_out[v] = g->owner[v] == 1 ? succ[v] : -2;
+    og_copy_out(g, &V, val, top, NULL, g->n_int);
+    if (inner_iters) *inner_iters = rounds;
     og_free_vals(&V);
     free(succ);
     return rc;

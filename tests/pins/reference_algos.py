@@ -78,8 +78,9 @@ def _add_unit(val, i, D):
     return tuple(c)
 
 
-def bellman_ford_br(owner, prio, adj, sigma, D):
-    """val^σ via Bellman-Ford relaxation from ⊤."""
+def bellman_ford_br(owner, prio, adj, sigma, D, return_rounds=False):
+    """val^σ via Bellman-Ford relaxation from ⊤. With return_rounds,
+    also the number of synchronous rounds computed (the last one changes nothing)."""
     n = len(owner)
     index = {p: i for i, p in enumerate(D)}
     zero = tuple([0] * len(D))
@@ -88,7 +89,7 @@ def bellman_ford_br(owner, prio, adj, sigma, D):
     def get(u):
         return zero if u == SINK else val[u]
 
-    for _ in range(n + 2):
+    for rnd in range(n + 2):
         changed = False
         new = list(val)
         for v in range(n):
@@ -105,7 +106,7 @@ def bellman_ford_br(owner, prio, adj, sigma, D):
             new[v] = nv
         val = new
         if not changed:
-            return val
+            return (val, rnd + 1) if return_rounds else val
     raise AssertionError("Bellman-Ford did not converge: negative (odd) cycle")
 
 

@@ -343,3 +343,94 @@ def test_ties_never_switch():
     tau, _, _, inner = Oracle(g).best_response(np.array([0, -1, -1], np.int32),
                                                np.array([2, 0, 0], np.int32))
     assert tau[0] == 2 and inner == 1
+
+
+# ------------------------------- SI-Reset and Bellman-Ford arms (§8(f) F2)
+@pytest.mark.parametrize("seed", range(40))
+def test_bf_best_response_matches_reference_bf(seed):
+    """Oracle BF best response vs the independent Python
+    Bellman-Ford: same val^σ, same round count (synchronous rounds from ⊤, the
+    last changing nothing: reading 19), τ = first ⊑-minimal successor at the
+    fixpoint (reading 3), no Odd-switchable edge under τ."""
+    rng = np.random.default_rng(17000 + seed)
+    n = int(rng.integers(2, 40))
+    g = gi.random_game(n, int(rng.integers(1, 7)), 1, min(4, n), seed)
+    o = Oracle(g)
+    owner, prio, adj, D, _ = _internal(o)
+    _, _, _, traj = ref.si_with_bellman_ford(owner, prio, adj, D)
+    for sigma in traj[:4]:
+        s = [x if x is not None else 0 for x in sigma]
+        tau, val, top, rounds = o.best_response_bf(np.array(s, np.int32))
+        bf, bf_rounds = ref.bellman_ford_br(owner, prio, adj, s, D, return_rounds=True)
+        assert _vals_from_oracle(val, top) == bf
+        assert rounds == bf_rounds
+        for v in range(o.n_internal):
+            if owner[v] == 1:
+                first = min((u for u in adj[v]), key=lambda u: (
+                    sum(ref.leq_strict(bf[w], bf[u], D) for w in adj[v]), adj[v].index(u)))
+                assert int(tau[v]) == first
+                assert not any(ref.leq_strict(bf[u], bf[int(tau[v])], D) for u in adj[v])
+        # val^σ is unique (PAPER.md:392-394): SI's best response has the same values
+        _, sval, stop, _ = o.best_response(np.array(s, np.int32))
+        assert _vals_from_oracle(sval, stop) == bf
+
+
+@pytest.mark.parametrize("seed", range(40))
+@pytest.mark.parametrize("mode", ["si_reset", "bf"])
+def test_arms_share_the_sigma_trajectory(seed, mode):
+    """val^σ is unique, so All_Even sees the same values whatever computes the best
+    response: SI-Reset and BF have SI's σ trajectory, outer
+    passes ("the number of major iterations does not depend on the algorithm used to
+    compute best responses"), σ*, W and val^{σ*}; and the
+    BF-driven reference SI agrees."""
+    rng = np.random.default_rng(19000 + seed)
+    n = int(rng.integers(2, 50))
+    g = gi.random_game(n, int(rng.integers(1, 8)), 1, min(5, n), seed)
+    o = Oracle(g)
+    owner, prio, adj, D, _ = _internal(o)
+    a = o.solve()
+    b = o.solve(mode=mode)
+    assert b.outer_passes == a.outer_passes
+    assert (b.even_trace == a.even_trace).all()
+    assert (b.winner == a.winner).all() and (b.sigma == a.sigma).all()
+    assert (b.top_int == a.top_int).all() and (b.val_int == a.val_int).all()
+    sig_star, outer, val, _ = ref.si_with_bellman_ford(owner, prio, adj, D)
+    assert outer == b.outer_passes
+    assert _vals_from_oracle(b.val_int, b.top_int) == val
+    if mode == "si_reset":
+        # every best response restarts from τ_init: the inner count is the sum of
+        # independent best responses along the σ trajectory
+        _, _, _, traj = ref.si_with_bellman_ford(owner, prio, adj, D)
+        tot = 0
+        for sigma in traj:
+            _, _, _, it = o.best_response(np.array([x if x is not None else 0 for x in sigma], np.int32))
+            tot += it
+        assert b.inner_iters == tot
+    else:
+        _, _, _, traj = ref.si_with_bellman_ford(owner, prio, adj, D)
+        tot = sum(ref.bellman_ford_br(owner, prio, adj, [x if x is not None else 0 for x in s], D,
+                                      return_rounds=True)[1] for s in traj)
+        assert b.inner_iters == tot
+
+
+def test_bf_closed_form_oddchain():
+    """F_oddchain(L) under Bellman-Ford: o_i's value settles in round
+    i+1 (its successor o_{i-1} settles one round earlier; round 1 settles the x_i and
+    g), so one best response of L+2 rounds (the last changes nothing); outer = 1;
+    τ*(o_i) = o_{i-1} and val(o_i) = {0:i, 1:1} as under SI."""
+    for L in (1, 2, 5, 30):
+        r = Oracle(gi.f_oddchain(L)).solve(mode="bf")
+        assert r.outer_passes == 1 and r.inner_iters == L + 2
+        for i in range(1, L + 1):
+            assert r.tau[L + i] == (L if i == 1 else L + i - 1)
+            assert list(r.val[L + i]) == [i, 1, 0]
+
+
+def test_bf_no_preprocess_inadmissible():
+    """An Odd-controlled odd cycle that reaches the sink is a negative cycle: BF
+    does not converge (reading 19)."""
+    g = gi.from_adjacency([1, 1, 0], [3, 1, 2], [[1, 2], [0], [2]])
+    o = Oracle(g, preprocess=False)
+    with pytest.raises(OracleError) as e:
+        o.solve(mode="bf")
+    assert e.value.name == "EINADMISSIBLE"
