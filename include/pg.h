@@ -85,9 +85,20 @@ enum {
                                  incremental valuation; results are identical)          */
     PG_HOST_LOAD = 32,        /* run pg_load's transform on the host (pg_load.cpp) instead
                                  of the GPU (pg_load_dev.cu); results are identical      */
-    PG_BFS = 64               /* full valuations by top-down BFS over the functional forest
+    PG_BFS = 64,              /* full valuations by top-down BFS over the functional forest
                                  (§V-bfs) instead of pointer jumping + walks; identical
                                  results, slower on B200 (scattered small writes)        */
+    /* Best-response arms of the paper's Table 2.
+     * Both leave W, σ*, val^{σ*}, the σ trajectory and outer_passes unchanged: val^σ
+     * is unique, so All_Even sees the same values.            */
+    PG_SI_RESET = 128,        /* SI-Reset: τ := τ_init (first successor) before every best
+                                 response instead of warm-starting from the previous one
+                                                                       */
+    PG_BELLMAN_FORD = 256     /* best responses by Bellman-Ford:
+                                 synchronous relaxation rounds from ⊤ until a round changes
+                                 nothing; inner_iters counts rounds; τ = first ⊑-minimal
+                                 successor at the fixpoint (reading 19). Takes
+                                 precedence over PG_SI_RESET                              */
 };
 
 typedef struct {
@@ -144,6 +155,14 @@ typedef struct {
     double ms_dist;          /* host wall time inside the exchange callback                 */
     int64_t prefix_gathers;  /* 32 B prefix gathers of the switch steps after an undecided
                                 8 B switch-key compare (DESIGN.md §4 switch keys)          */
+    /* PG_BELLMAN_FORD arm */
+    int64_t bf_rounds;       /* relaxation rounds (= inner_iters of a BF solve)             */
+    double ms_bf;            /* PG_PHASE_TIMING: CUDA-event total of the rounds             */
+    int64_t n_bf;
+    double bytes_bf;         /* algorithmic bytes of the rounds: per vertex pidx + ⊤ read +
+                                ⊤ write (3 B), CSR offsets / σ (4 B per Odd offset or Even σ),
+                                per Odd edge its target and ⊤ flag (5 B), τ write (4 B per Odd),
+                                and R bytes per finite row gathered, compared or written     */
 } pg_stats;
 
 /* pg_load: validate, canonicalise and preprocess a game, copy it to the GPU.
@@ -184,8 +203,10 @@ pg_status pg_valuate(pg_game g, const int32_t *strategy, int32_t *val, uint8_t *
  *                successor (reading 4)
  *   tau_out      int32[n_internal] or NULL: τ at exit (PG_NONE at Even vertices)
  *   val, top     as pg_valuate, for the profile (σ, τ_out), i.e. val^σ
- *   inner_iters  int64* or NULL: valuations computed
- * Errors: PG_EINVAL, PG_EINADMISSIBLE (odd cycle reached), PG_EITERCAP. */
+ *   inner_iters  int64* or NULL: valuations computed (relaxation rounds with
+ *                PG_BELLMAN_FORD, which ignores tau0)
+ * Errors: PG_EINVAL, PG_EINADMISSIBLE (odd cycle reached; with PG_BELLMAN_FORD also
+ * no convergence within n_internal + 1 rounds), PG_EITERCAP. */
 pg_status pg_best_response(pg_game g, const int32_t *sigma, const int32_t *tau0,
                            int32_t *tau_out, int32_t *val, uint8_t *top,
                            int64_t *inner_iters);

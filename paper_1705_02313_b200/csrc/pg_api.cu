@@ -19,7 +19,7 @@ static thread_local std::string t_err;
 
 static void set_err(const std::string &s) { t_err = s; }
 
-enum Phase { PH_V1 = 0, PH_V2, PH_ODD, PH_EVEN, PH_OTHER, PH_INC, PH_BFS, PH_N };
+enum Phase { PH_V1 = 0, PH_V2, PH_ODD, PH_EVEN, PH_OTHER, PH_INC, PH_BFS, PH_BF, PH_N };
 
 struct pg_game_s {
     int device = 0;
@@ -64,6 +64,9 @@ struct pg_game_s {
     int2 *swl_all = nullptr;          // world × max(|S_r|) gathered switch lists
     size_t swl_all_cap = 0;
     int64_t *h_x = nullptr;           // pinned scratch (exchange counts, total |S|)
+    // Bellman-Ford arm (PG_BELLMAN_FORD): double-buffered key rows and ⊤ flags
+    int32_t *bf_row[2] = {nullptr, nullptr};
+    uint8_t *bf_top[2] = {nullptr, nullptr};
 };
 
 #define CK(h, x)                                                                         \
@@ -155,6 +158,7 @@ void timing_collect(pg_game h) {
             case PH_EVEN: h->st.ms_even += ms; h->st.n_even++; break;
             case PH_INC: h->st.ms_inc += ms; h->st.n_inc++; break;
             case PH_BFS: h->st.ms_bfs += ms; h->st.n_bfs++; break;
+            case PH_BF: h->st.ms_bf += ms; h->st.n_bf++; break;
             default: h->st.ms_other += ms; break;
         }
     }
@@ -472,6 +476,80 @@ pg_status inner_loop(pg_game h, int64_t *inner, bool check) {
         }
         if (so.sw_last == 0) return PG_OK;
     }
+}
+
+// Bellman-Ford best response: synchronous
+// relaxation rounds (k_bf_round) from val ≡ ⊤ until a round changes nothing
+// (reading 19); every round also writes τ(v) = the first ⊑-minimal
+// successor, final after the last round. The profile (σ, τ) is then valuated from
+// scratch so that All_Even and the outputs see the usual compact prefixes; its
+// values equal the fixpoint (a ⊑-minimal choice closes no cycle among finite
+// vertices, and ⊤ vertices only reach ⊤ vertices).
+pg_status bf_inner(pg_game h, int64_t *inner, bool check) {
+    const size_t N1 = (size_t)h->G.n_int + 1;
+    if (!h->bf_row[0]) {
+        for (int b = 0; b < 2; b++) {
+            CK(h, dalloc(h, &h->bf_row[b], N1 * h->G.dp));
+            CK(h, dalloc(h, &h->bf_top[b], N1));
+        }
+    }
+    CK(h, cudaMemsetAsync(h->bf_top[0], 1, N1, h->stream));   // val ≡ ⊤ (the sink is never read)
+    const double np_ = (double)h->G.n_int, no = (double)(h->G.n_int - h->G.n_even);
+    const double R = 4.0 * h->G.dp;
+    int cur = 0;
+    for (int64_t r = 0;; r++) {
+        if (r > h->G.n_int + 1) {
+            set_err("Bellman-Ford did not converge: odd cycle reached (strategy not admissible)");
+            return PG_EINADMISSIBLE;
+        }
+        if (h->max_inner > 0 && *inner >= h->max_inner) {
+            set_err("inner iteration cap reached");
+            return PG_EITERCAP;
+        }
+        CK(h, cudaMemsetAsync(&h->G.ctl->bf_changed, 0, 2 * sizeof(unsigned long long), h->stream));
+        {
+            PhaseScope ps(h, PH_BF);
+            CK(h, launch_bf_round(h->G, h->lc.sms, h->bf_row[cur], h->bf_top[cur], h->bf_row[cur ^ 1],
+                                  h->bf_top[cur ^ 1], &h->G.ctl->bf_changed, &h->G.ctl->bf_rows, h->stream));
+        }
+        h->st.gpu_launches += 1;
+        CK(h, cudaMemcpyAsync(&h->h_ctl->bf_changed, &h->G.ctl->bf_changed, 2 * sizeof(unsigned long long),
+                              cudaMemcpyDeviceToHost, h->stream));
+        CK(h, cudaStreamSynchronize(h->stream));
+        (*inner)++;
+        h->st.bf_rounds++;
+        // pidx + own ⊤ + ⊤ write, σ / CSR offsets, per Odd edge target + ⊤ flag, τ write,
+        // and the finite rows gathered, compared and written
+        h->st.bytes_bf += 3.0 * np_ + 4.0 * (np_ + 1) + 5.0 * (double)h->m_odd + 4.0 * no +
+                          R * (double)h->h_ctl->bf_rows;
+        cur ^= 1;
+        if (h->h_ctl->bf_changed == 0) break;
+    }
+    h->have_state = false;
+    for (;;) {   // valuation of (σ, τ): compact prefixes for All_Even, odd-cycle check
+        pg_status rc = valuate_dev(h, check, false);
+        if (rc) return rc;
+        if ((rc = readback(h))) return rc;
+        if (!h->h_ctl->spl_overflow) break;
+        if ((rc = grow_splitters(h, (int64_t)h->h_ctl->nspl))) return rc;
+    }
+    note_valuation(h, false, false);
+    h->have_state = true;
+    h->last_inc = false;
+    h->c_valid = false;
+    h->last_nsw = 0;
+    h->last_maxdepth = (int64_t)h->h_ctl->maxdepth;
+    if (check && h->h_ctl->odd_cycle) {
+        set_err("odd cycle reached: strategy not admissible");
+        return PG_EINADMISSIBLE;
+    }
+    return PG_OK;
+}
+
+// Best response of Algorithm 1's inner loop or of the Table 2 arms.
+pg_status best_response_dev(pg_game h, int64_t *inner, bool check) {
+    if (h->flags & PG_BELLMAN_FORD) return bf_inner(h, inner, check);
+    return inner_loop(h, inner, check);
 }
 
 // All_Even. Incremental over C when every valuation
@@ -922,7 +1000,7 @@ pg_status pg_best_response(pg_game h, const int32_t *sigma, const int32_t *tau0,
     if (N) {
         if ((rc = import_strategy(h, sigma, tau0 ? 1 : 1 | 4))) return rc;
         if (tau0 && (rc = import_strategy(h, tau0, 2))) return rc;
-        rc = inner_loop(h, &inner, true);   // arbitrary σ: always check admissibility
+        rc = best_response_dev(h, &inner, true);   // arbitrary σ: always check admissibility
         if (inner_iters) *inner_iters = inner;
         h->st.inner_iters = inner;
         if (rc) return rc;
@@ -967,7 +1045,14 @@ pg_status pg_solve(pg_game h, uint8_t *winner, int32_t *sigma, int32_t *tau, int
                 rc = PG_EITERCAP;
                 break;
             }
-            rc = inner_loop(h, &inner, check);               // τ := br(σ), warm-started
+            if ((h->flags & PG_SI_RESET) && outer > 0) {     // SI-Reset: τ := τ_init
+                PhaseScope ps(h, PH_OTHER);
+                CK(h, launch_import_strategy(h->G, nullptr, 4, h->stream));
+                h->st.gpu_launches += 1;
+                h->have_state = false;
+                h->c_valid = false;
+            }
+            rc = best_response_dev(h, &inner, check);        // τ := br(σ), warm-started
             if (rc) break;
             outer++;
             int64_t c = 0;

@@ -69,6 +69,8 @@ struct Ctl {
     unsigned long long nhard;       // vertices deferred to the hard (full-compare) pass
     unsigned long long nswl;        // switches of the last switch step (must follow nhard); = |S|
     unsigned long long nC;          // |C|: vertices in some dirty set since the last All_Even
+    unsigned long long bf_changed;  // Bellman-Ford round: vertices whose value changed
+    unsigned long long bf_rows;     // ... finite rows gathered, compared or written
     unsigned int bar_count;         // grid barrier
     unsigned int bar_gen;
     unsigned long long ts[12];      // PGSI_TRACE=2: %globaltimer at the incremental kernel's phase ends
@@ -158,6 +160,9 @@ cudaError_t launch_even_inc(const DevGame &g, cudaStream_t s);
 cudaError_t launch_apply_all(const DevGame &g, cudaStream_t s);   // σ[S]/τ[S] of the exchanged S
 cudaError_t launch_val_bfs(const DevGame &g, const LaunchCfg &lc, cudaStream_t s);
 size_t children_scan_bytes(int64_t n1);
+// Bellman-Ford arm (pg_bf.cu): one synchronous relaxation round cur -> nxt
+cudaError_t launch_bf_round(const DevGame &g, int sms, const int32_t *cur, const uint8_t *tcur, int32_t *nxt,
+                            uint8_t *tnxt, unsigned long long *changed, unsigned long long *rows, cudaStream_t s);
 cudaError_t launch_export_val(const DevGame &g, int64_t count, int32_t *val_out, uint8_t *top_out,
                               cudaStream_t s);
 cudaError_t launch_export_strategy(const DevGame &g, int64_t count, int32_t *out, int which,

@@ -28,6 +28,9 @@ PG_PTRS_ON_DEVICE = 8
 PG_NO_INCREMENTAL = 16
 PG_HOST_LOAD = 32
 PG_BFS = 64
+PG_SI_RESET = 128
+PG_BELLMAN_FORD = 256
+BEST_RESPONSE = {"si": 0, "si_reset": PG_SI_RESET, "bf": PG_BELLMAN_FORD}
 
 STATUS = {0: "PG_OK", -1: "PG_EINVAL", -2: "PG_ENOMEM", -3: "PG_ECUDA", -4: "PG_ENCCL",
           -5: "PG_EINADMISSIBLE", -6: "PG_EITERCAP", -7: "PG_ESTATE", -8: "PG_ENOTSUP"}
@@ -62,7 +65,8 @@ class Stats(C.Structure):
         ("ms_inc", C.c_double),
         ("n_inc", C.c_int64), ("bytes_inc", C.c_double),
         ("dist_exchanges", C.c_int64), ("dist_bytes", C.c_int64), ("ms_dist", C.c_double),
-        ("prefix_gathers", C.c_int64)]
+        ("prefix_gathers", C.c_int64),
+        ("bf_rounds", C.c_int64), ("ms_bf", C.c_double), ("n_bf", C.c_int64), ("bytes_bf", C.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -126,14 +130,16 @@ class Game:
                  preprocess: bool = True, check: bool = False, phase_timing: bool = False,
                  device_ptrs: bool = False, splitter_k: int = 0, max_inner: int = 0,
                  max_outer: int = 0, prefix_pairs: int = 0, incremental: bool = True,
-                 host_load: bool = False, bfs: bool = False):
+                 host_load: bool = False, bfs: bool = False, best_response: str = "si"):
+        """best_response: "si" (Algorithm 1), "si_reset" (PG_SI_RESET) or "bf"
+        (PG_BELLMAN_FORD), the arms of the paper's Table 2."""
         L = load_library()
         self._in = (np.ascontiguousarray(row_ptr, np.int64), np.ascontiguousarray(col, np.int32),
                     np.ascontiguousarray(owner, np.uint8), np.ascontiguousarray(priority, np.int32))
         flags = ((0 if preprocess else PG_NO_PREPROCESS) | (PG_CHECK_INVARIANTS if check else 0) |
                  (PG_PHASE_TIMING if phase_timing else 0) | (PG_PTRS_ON_DEVICE if device_ptrs else 0) |
                  (0 if incremental else PG_NO_INCREMENTAL) | (PG_HOST_LOAD if host_load else 0) |
-                 (PG_BFS if bfs else 0))
+                 (PG_BFS if bfs else 0) | BEST_RESPONSE[best_response])
         opt = Options(flags, device, C.c_void_p(stream) if stream else None, splitter_k,
                       prefix_pairs, max_inner, max_outer)
         h = C.c_void_p()
