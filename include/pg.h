@@ -159,10 +159,11 @@ typedef struct {
     int64_t bf_rounds;       /* relaxation rounds (= inner_iters of a BF solve)             */
     double ms_bf;            /* PG_PHASE_TIMING: CUDA-event total of the rounds             */
     int64_t n_bf;
-    double bytes_bf;         /* algorithmic bytes of the rounds: per vertex pidx + ⊤ read +
-                                ⊤ write (3 B), CSR offsets / σ (4 B per Odd offset or Even σ),
-                                per Odd edge its target and ⊤ flag (5 B), τ write (4 B per Odd),
-                                and R bytes per finite row gathered, compared or written     */
+    double bytes_bf;         /* algorithmic bytes of the rounds: per vertex pidx (1 B) and
+                                CSR offset / σ (4 B), per Odd edge its target (4 B), τ write
+                                (4 B per Odd vertex), and R = 4·dp bytes per row gathered
+                                (candidates, the vertex's previous row) or written (finite
+                                new rows; ⊤ is encoded in the row)                          */
 } pg_stats;
 
 /* pg_load: validate, canonicalise and preprocess a game, copy it to the GPU.

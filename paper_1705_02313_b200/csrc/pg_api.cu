@@ -64,9 +64,8 @@ struct pg_game_s {
     int2 *swl_all = nullptr;          // world × max(|S_r|) gathered switch lists
     size_t swl_all_cap = 0;
     int64_t *h_x = nullptr;           // pinned scratch (exchange counts, total |S|)
-    // Bellman-Ford arm (PG_BELLMAN_FORD): double-buffered key rows and ⊤ flags
+    // Bellman-Ford arm (PG_BELLMAN_FORD): double-buffered key rows (⊤ = all INT_MAX)
     int32_t *bf_row[2] = {nullptr, nullptr};
-    uint8_t *bf_top[2] = {nullptr, nullptr};
 };
 
 #define CK(h, x)                                                                         \
@@ -487,13 +486,11 @@ pg_status inner_loop(pg_game h, int64_t *inner, bool check) {
 // vertices, and ⊤ vertices only reach ⊤ vertices).
 pg_status bf_inner(pg_game h, int64_t *inner, bool check) {
     const size_t N1 = (size_t)h->G.n_int + 1;
-    if (!h->bf_row[0]) {
-        for (int b = 0; b < 2; b++) {
-            CK(h, dalloc(h, &h->bf_row[b], N1 * h->G.dp));
-            CK(h, dalloc(h, &h->bf_top[b], N1));
-        }
-    }
-    CK(h, cudaMemsetAsync(h->bf_top[0], 1, N1, h->stream));   // val ≡ ⊤ (the sink is never read)
+    if (!h->bf_row[0])
+        for (int b = 0; b < 2; b++) CK(h, dalloc(h, &h->bf_row[b], N1 * h->G.dp));
+    // val ≡ ⊤ in both buffers (⊤ rows are never rewritten; the sink row is never read)
+    CK(h, launch_bf_init(h->bf_row[0], h->bf_row[1], (int64_t)N1 * h->G.dp, h->lc.sms, h->stream));
+    h->st.gpu_launches += 2;
     const double np_ = (double)h->G.n_int, no = (double)(h->G.n_int - h->G.n_even);
     const double R = 4.0 * h->G.dp;
     int cur = 0;
@@ -509,8 +506,8 @@ pg_status bf_inner(pg_game h, int64_t *inner, bool check) {
         CK(h, cudaMemsetAsync(&h->G.ctl->bf_changed, 0, 2 * sizeof(unsigned long long), h->stream));
         {
             PhaseScope ps(h, PH_BF);
-            CK(h, launch_bf_round(h->G, h->lc.sms, h->bf_row[cur], h->bf_top[cur], h->bf_row[cur ^ 1],
-                                  h->bf_top[cur ^ 1], &h->G.ctl->bf_changed, &h->G.ctl->bf_rows, h->stream));
+            CK(h, launch_bf_round(h->G, h->lc.sms, h->bf_row[cur], h->bf_row[cur ^ 1], &h->G.ctl->bf_changed,
+                                  &h->G.ctl->bf_rows, h->stream));
         }
         h->st.gpu_launches += 1;
         CK(h, cudaMemcpyAsync(&h->h_ctl->bf_changed, &h->G.ctl->bf_changed, 2 * sizeof(unsigned long long),
@@ -518,9 +515,9 @@ pg_status bf_inner(pg_game h, int64_t *inner, bool check) {
         CK(h, cudaStreamSynchronize(h->stream));
         (*inner)++;
         h->st.bf_rounds++;
-        // pidx + own ⊤ + ⊤ write, σ / CSR offsets, per Odd edge target + ⊤ flag, τ write,
-        // and the finite rows gathered, compared and written
-        h->st.bytes_bf += 3.0 * np_ + 4.0 * (np_ + 1) + 5.0 * (double)h->m_odd + 4.0 * no +
+        // pidx, σ / CSR offsets, per Odd edge its target, τ write, and the rows gathered
+        // (candidates, the previous own row) and written (finite new rows)
+        h->st.bytes_bf += 1.0 * np_ + 4.0 * (np_ + 1) + 4.0 * (double)h->m_odd + 4.0 * no +
                           R * (double)h->h_ctl->bf_rows;
         cur ^= 1;
         if (h->h_ctl->bf_changed == 0) break;

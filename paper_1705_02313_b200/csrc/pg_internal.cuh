@@ -161,8 +161,9 @@ cudaError_t launch_apply_all(const DevGame &g, cudaStream_t s);   // σ[S]/τ[S]
 cudaError_t launch_val_bfs(const DevGame &g, const LaunchCfg &lc, cudaStream_t s);
 size_t children_scan_bytes(int64_t n1);
 // Bellman-Ford arm (pg_bf.cu): one synchronous relaxation round cur -> nxt
-cudaError_t launch_bf_round(const DevGame &g, int sms, const int32_t *cur, const uint8_t *tcur, int32_t *nxt,
-                            uint8_t *tnxt, unsigned long long *changed, unsigned long long *rows, cudaStream_t s);
+cudaError_t launch_bf_round(const DevGame &g, int sms, const int32_t *cur, int32_t *nxt,
+                            unsigned long long *changed, unsigned long long *rows, cudaStream_t s);
+cudaError_t launch_bf_init(int32_t *rows0, int32_t *rows1, int64_t count, int sms, cudaStream_t s);
 cudaError_t launch_export_val(const DevGame &g, int64_t count, int32_t *val_out, uint8_t *top_out,
                               cudaStream_t s);
 cudaError_t launch_export_strategy(const DevGame &g, int64_t count, int32_t *out, int which,
