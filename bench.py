@@ -56,6 +56,22 @@ THROTTLE_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_p
                  0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
 
 
+def ncu_traffic(kernel_prefix):
+    """DRAM bytes per launch of a kernel from the committed ncu launch list of this
+    round (profiles/r1/kernel_traffic.json, written by scripts/traffic_json.py from
+    `ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,...` over one bench
+    solve; cold-cache, serialised launches). None if not profiled."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1", "kernel_traffic.json")
+    try:
+        data = json.load(open(path))
+    except (OSError, ValueError):
+        return None, None
+    for k, v in data.get("kernels", {}).items():
+        if k.replace("void ", "").startswith(kernel_prefix):
+            return v["dram_bytes_per_launch"], "profiles/r1/kernel_traffic.json (ncu launch list, per-launch mean)"
+    return None, None
+
+
 def measured_peak_gbs():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -186,6 +202,7 @@ def main():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-arms", action="store_true", help="skip the SI-Reset / Bellman-Ford arms")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e/cpu/clocks)")
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
@@ -258,8 +275,11 @@ def main():
     dms, dbytes, dn = phases[dom]
     achieved = dbytes / (dms / 1000.0) / 1e9 if dms > 0 else 0.0
     total_phase_ms = sum(v[0] for v in phases.values()) + acc["ms_other"]
+    kname = {"v1": "k_v1", "v2": "k_v2_cpx", "inc": "k_inc_iter", "bfs": "k_val_bfs",
+             "odd": "k_switch<1, 0>", "even": "k_switch<0, 0>"}[dom]
+    traffic, traffic_src = ncu_traffic(kname)
     roofline = {"bound": "hbm", "kernel": kern[dom], "achieved": achieved, "peak": peak,
-                "unit": "GB/s", "frac": achieved / peak, "traffic": None,
+                "unit": "GB/s", "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
                 "bytes_per_launch": dbytes / max(dn, 1), "ms_per_launch": dms / max(dn, 1),
                 "share_of_step": dms / total_phase_ms if total_phase_ms else None,
                 "peak_source": peak_src,
@@ -287,6 +307,43 @@ def main():
         scratch = {"value": s_units / (sms / 1000.0), "ms_per_step": sms / args.steps,
                    "note": "PG_NO_INCREMENTAL: every valuation recomputed for all vertices"}
         Gs.free()
+
+    # ---- best-response arms of the paper's Table 2 on
+    # the same game: SI-Reset and Bellman-Ford. Same σ trajectory and outer passes (val^σ
+    # is unique); the iteration counts and times differ. One untimed + one timed solve each.
+    arms = None
+    if not args.profile and not args.no_arms:
+        arms = {}
+        for arm in ("si_reset", "bf"):
+            Ga = Game.from_game(game, device=local, stream=stream.cuda_stream, device_ptrs=True,
+                                phase_timing=True, best_response=arm)
+            Ga.solve(out=out)
+            barrier()
+            torch.cuda.synchronize(dev)
+            e0.record(stream)
+            ra = Ga.solve(out=out)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            ams = e0.elapsed_time(e1)
+            st = ra.stats
+            a = {"solve_ms": ams, "inner_iters": st["inner_iters"], "outer_passes": st["outer_passes"],
+                 "iters_vs_si": st["inner_iters"] / max(inner, 1),
+                 "time_vs_si": ams / (ms / args.steps)}
+            if arm == "bf":
+                bf_ms, bf_bytes, bf_n = st["ms_bf"], st["bytes_bf"], st["n_bf"]
+                ach = bf_bytes / (bf_ms / 1000.0) / 1e9 if bf_ms else 0.0
+                a["iters_unit"] = "relaxation rounds"
+                tr, tr_src = ncu_traffic("k_bf_round")
+                a["roofline"] = {"bound": "hbm", "kernel": "k_bf_round (one Bellman-Ford relaxation round)",
+                                 "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                                 "traffic": tr, "traffic_source": tr_src,
+                                 "bytes_per_launch": bf_bytes / max(bf_n, 1),
+                                 "ms_per_launch": bf_ms / max(bf_n, 1), "launches": bf_n,
+                                 "share_of_arm": bf_ms / ams if ams else None}
+            else:
+                a["iters_unit"] = "valuations"
+            arms[arm] = a
+            Ga.free()
 
     # ---- end to end through the public API, pinned host buffers
     e2e = None
@@ -351,6 +408,7 @@ def main():
                              f"(prefixes, jl, succ, pidx, ⊤, CSR) > 126 MB; no flush needed"},
             "roofline": roofline,
             "from_scratch": scratch,
+            "arms": arms,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": sampler.summary(),
