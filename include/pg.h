@@ -270,6 +270,43 @@ typedef int (*pg_allgather_fn)(void *ctx, const void *send, void *recv, int64_t 
 pg_status pg_dist_attach(pg_game g, int32_t rank, int32_t world, pg_allgather_fn fn,
                          void *ctx);
 
+/* ---- PGSolver interchange and solution verification (host-side
+ * native code, no GPU, no handle) ------------------------------------------------ */
+
+/* pg_parse_pgsolver: parse a game in PGSolver format: optional header
+ * `parity <maxid>;` (and `start <id>;`, ignored), then one statement per vertex
+ * `<id> <priority> <owner> <succ>,<succ>,... ["name"];`, owner 0 = Even, 1 = Odd.
+ * Output is the CSR pg_load takes, successor order as written. Two-call pattern:
+ * pass NULL arrays to get n and m, then buffers of n+1 / m / n / n entries.
+ *   text, len     the bytes (not NUL-terminated necessarily)
+ * Errors: PG_EINVAL with "line L, column C" for a syntax error, a vertex without
+ * successors, a duplicate or missing vertex, an out-of-range successor or owner. */
+pg_status pg_parse_pgsolver(const char *text, int64_t len, int64_t *n, int64_t *m, int64_t *row_ptr,
+                            int32_t *col, uint8_t *owner, int32_t *priority);
+
+/* pg_format_solution: PGSolver solution text: `paritysol <n-1>;`
+ * then `<v> <winner> [<succ>];` per vertex, the successor only where the vertex's
+ * owner is its winner (σ* for Even, τ* for Odd; pg_solve's outputs).
+ *   buf, cap      NULL to query *len (bytes without the NUL); else cap >= *len + 1
+ * Errors: PG_EINVAL (NULL argument, buffer too small). */
+pg_status pg_format_solution(int64_t n, const uint8_t *owner, const uint8_t *winner, const int32_t *sigma,
+                             const int32_t *tau, char *buf, int64_t cap, int64_t *len);
+
+/* pg_verify_solution: check a claimed solution against the definition of winning
+ * (Thm 1), independently of the
+ * solver. For each player i: (a) closure — i's strategy edges (σ for Even, τ for Odd,
+ * at vertices i owns in W_i) are edges into W_i, and every edge of an opponent vertex
+ * in W_i stays in W_i; (b) parity — in the one-player graph on W_i no cycle has a
+ * maximum priority of the opponent's parity (per priority p: no cycle through a
+ * priority-p vertex among the vertices of priority <= p; Tarjan SCC, host C++).
+ * Inputs are the ORIGINAL game (as given to pg_load) and pg_solve's outputs (host).
+ *   witness      int64* or NULL: a vertex where the check failed, -1 if valid
+ * Returns PG_OK if the solution is correct, PG_EINVAL (message names the failing
+ * check) otherwise. */
+pg_status pg_verify_solution(int64_t n, const int64_t *row_ptr, const int32_t *col, const uint8_t *owner,
+                             const int32_t *priority, const uint8_t *winner, const int32_t *sigma,
+                             const int32_t *tau, int64_t *witness);
+
 /* pg_get_stats: statistics of the last call on the handle (host pointer). */
 pg_status pg_get_stats(pg_game g, pg_stats *stats);
 

@@ -18,6 +18,9 @@ using namespace pgsi;
 static thread_local std::string t_err;
 
 static void set_err(const std::string &s) { t_err = s; }
+namespace pgsi {
+void io_set_err(const std::string &s) { t_err = s; }   // pg_io.cpp
+}
 
 enum Phase { PH_V1 = 0, PH_V2, PH_ODD, PH_EVEN, PH_OTHER, PH_INC, PH_BFS, PH_BF, PH_N };
 

@@ -98,6 +98,11 @@ def load_library(path: str = LIB_PATH):
     for f in ("pg_load", "pg_info", "pg_valuate", "pg_best_response", "pg_solve", "pg_get_stats",
               "pg_inspect", "pg_dist_attach"):
         getattr(L, f).restype = C.c_int
+    L.pg_parse_pgsolver.argtypes = [C.c_char_p, C.c_int64, P, P, P, P, P, P]
+    L.pg_format_solution.argtypes = [C.c_int64, P, P, P, P, C.c_char_p, C.c_int64, P]
+    L.pg_verify_solution.argtypes = [C.c_int64, P, P, P, P, P, P, P, P]
+    for f in ("pg_parse_pgsolver", "pg_format_solution", "pg_verify_solution"):
+        getattr(L, f).restype = C.c_int
     L.pg_free.argtypes = [C.c_void_p]
     L.pg_free.restype = None
     L.pg_last_error.restype = C.c_char_p
@@ -280,3 +285,68 @@ def inspect(g, preprocess: bool = True):
 
 def version() -> str:
     return load_library().pg_version().decode()
+
+
+@dataclass
+class ParsedGame:
+    n: int
+    row_ptr: np.ndarray
+    col: np.ndarray
+    owner: np.ndarray
+    priority: np.ndarray
+
+    @property
+    def m(self):
+        return int(self.row_ptr[-1])
+
+
+def parse_pgsolver(text) -> ParsedGame:
+    """PGSolver text -> CSR game (``pg_parse_pgsolver``, host C++)."""
+    L = load_library()
+    b = text.encode() if isinstance(text, str) else bytes(text)
+    n, m = C.c_int64(), C.c_int64()
+    rc = L.pg_parse_pgsolver(b, len(b), C.byref(n), C.byref(m), None, None, None, None)
+    if rc:
+        raise PGError(rc, L.pg_last_error().decode())
+    rp = np.zeros(n.value + 1, np.int64)
+    col = np.zeros(max(m.value, 1), np.int32)
+    own = np.zeros(max(n.value, 1), np.uint8)
+    pri = np.zeros(max(n.value, 1), np.int32)
+    rc = L.pg_parse_pgsolver(b, len(b), None, None, _ptr(rp), _ptr(col), _ptr(own), _ptr(pri))
+    if rc:
+        raise PGError(rc, L.pg_last_error().decode())
+    return ParsedGame(n.value, rp, col[:m.value], own[:n.value], pri[:n.value])
+
+
+def format_solution(owner, winner, sigma, tau) -> str:
+    """PGSolver solution text (``pg_format_solution``)."""
+    L = load_library()
+    arrs = [np.ascontiguousarray(owner, np.uint8), np.ascontiguousarray(winner, np.uint8),
+            np.ascontiguousarray(sigma, np.int32), np.ascontiguousarray(tau, np.int32)]
+    n = len(arrs[0])
+    ln = C.c_int64()
+    rc = L.pg_format_solution(n, *[_ptr(a) for a in arrs], None, 0, C.byref(ln))
+    if rc:
+        raise PGError(rc, L.pg_last_error().decode())
+    buf = C.create_string_buffer(ln.value + 1)
+    rc = L.pg_format_solution(n, *[_ptr(a) for a in arrs], buf, ln.value + 1, C.byref(ln))
+    if rc:
+        raise PGError(rc, L.pg_last_error().decode())
+    return buf.value.decode()
+
+
+def verify_solution(g, winner, sigma, tau):
+    """(ok, witness, message) from ``pg_verify_solution`` on the original game g."""
+    L = load_library()
+    arrs = [np.ascontiguousarray(g.row_ptr, np.int64), np.ascontiguousarray(g.col, np.int32),
+            np.ascontiguousarray(g.owner, np.uint8), np.ascontiguousarray(g.priority, np.int32),
+            np.ascontiguousarray(winner, np.uint8), np.ascontiguousarray(sigma, np.int32),
+            np.ascontiguousarray(tau, np.int32)]
+    w = C.c_int64()
+    rc = L.pg_verify_solution(int(g.n), *[_ptr(a) for a in arrs], C.byref(w))
+    if rc == 0:
+        return True, -1, ""
+    if rc != -1:
+        raise PGError(rc, L.pg_last_error().decode())
+    return False, w.value, L.pg_last_error().decode()
+

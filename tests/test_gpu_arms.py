@@ -116,3 +116,25 @@ def test_arms_device_pointers(pg):
         np.testing.assert_array_equal(res.tau.cpu().numpy(), ora.tau)
         np.testing.assert_array_equal(res.val.cpu().numpy(), ora.val)
         torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("n,d,lo,hi", [(1_000_000, 16, 2, 5), (200_000, 40, 2, 5)])
+def test_full_size_solution_verifies(pg, n, d, lo, hi):
+    """BASELINE configs[1] at full size (and a wide-row game): the GPU solution of
+    every arm passes the independent verifier (closure + per-priority cycle check,
+    pg_verify_solution) — a property that holds at any size — and the arms agree
+    on W and σ* (val^σ is unique)."""
+    g = gi.random_game(n, d, lo, hi, 1)
+    base = None
+    for mode in ("si", "si_reset", "bf"):
+        G = pg.Game.from_game(g, best_response=mode)
+        res = G.solve()
+        ok, w, msg = pg.verify_solution(g, res.winner, res.sigma, res.tau)
+        assert ok, (mode, msg)
+        if base is None:
+            base = res
+        else:
+            np.testing.assert_array_equal(res.winner, base.winner)
+            np.testing.assert_array_equal(res.sigma, base.sigma)
+            assert res.stats["outer_passes"] == base.stats["outer_passes"]
+        G.free()
