@@ -42,7 +42,7 @@ for rep in sys.argv[3:]:
         b = sum(float(d[m]) * scale.get(u[m], 1) for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
         out.setdefault("full_set", {})[k] = {"capture": rep.split("/")[-1], "dram_bytes": b,
                                               "duration_ns": float(d["gpu__time_duration.sum"]) *
-                                              {"nsecond": 1, "usecond": 1e3, "msecond": 1e6}.get(
+                                              {"nsecond": 1, "ns": 1, "usecond": 1e3, "us": 1e3, "msecond": 1e6, "ms": 1e6}.get(
                                                   u["gpu__time_duration.sum"], 1)}
 json.dump(out, open(sys.argv[2], "w"), indent=1)
 print(json.dumps(out, indent=1)[:3000])

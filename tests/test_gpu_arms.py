@@ -2,8 +2,8 @@
 SI-Reset (PG_SI_RESET, PAPER.md:976-981) and Bellman-Ford (PG_BELLMAN_FORD,
 PAPER.md:494-504) through the C ABI vs the oracle's modes, bit-exact: winners,
 σ*, τ*, val^{σ*}, inner iterations (valuations resp. relaxation rounds) and outer
-passes. Row widths cover every k_bf_round instantiation: G = dp lanes per vertex
-for dp <= 32 (d = 1..32) and C = dp/32 column chunks per lane for d > 32."""
+passes. Row widths cover every k_bf_round instantiation (dp = 1, 2, 4..128 with
+16-byte vectors over G lanes, and the multi-chunk layouts of dp = 160..256)."""
 import numpy as np
 import pytest
 
