@@ -52,6 +52,7 @@ struct pg_game_s {
     // incremental valuation state
     bool have_state = false;     // jl / cpx / top describe the profile before the last switch list
     int64_t last_nsw = 0;        // size of the last switch list (S)
+    bool last_sw_odd = false;    // ... which came from All_Odd (true) or All_Even
     bool last_inc = false;
     uint32_t epoch = 0;
     bool trace = false;               // PGSI_TRACE=1 (debug)
@@ -237,6 +238,7 @@ pg_status valuate_dev(pg_game h, bool want_cdom, bool full_rows, bool inc = fals
         h->G.epoch = h->epoch + 1;
         h->epoch += steps;
         h->G.inc_max_steps = (int32_t)steps;
+        h->G.inc_s_odd = h->last_sw_odd ? 1 : 0;
         PhaseScope ps(h, PH_INC);
         CK(h, launch_inc_iter(h->G, h->lc, h->stream, h->last_nsw));
         h->st.gpu_launches += 1;
@@ -427,7 +429,10 @@ pg_status valuate_and_switch(pg_game h, bool odd, bool want_cdom, bool do_switch
         if (rc) return rc;
     }
     h->have_state = true;
-    if (do_switch) h->last_nsw = (int64_t)h->h_ctl->nswl;
+    if (do_switch) {
+        h->last_nsw = (int64_t)h->h_ctl->nswl;
+        h->last_sw_odd = odd;
+    }
     if (!inc) h->last_maxdepth = (int64_t)h->h_ctl->maxdepth;
     if (!inc) h->c_valid = false;   // a from-scratch valuation: C no longer covers the changes
     if (h->trace)
@@ -581,6 +586,7 @@ pg_status even_switch(pg_game h, int64_t *count) {
     if ((rc = dist_exchange(h, false))) return rc;
     *count = (int64_t)h->h_ctl->even_switches;
     h->last_nsw = (int64_t)h->h_ctl->nswl;
+    h->last_sw_odd = false;
     if (h->trace) fprintf(stderr, "[pgsi] even switch: inc=%d |C|=%llu |E|=%llu %lld switches\n", (int)inc,
                           h->h_ctl->nC, inc ? h->h_ctl->nE : 0ull, (long long)*count);
     h->st.even_switches += *count;
@@ -848,6 +854,8 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     G.inc_s_div = h->inc_s_div;
     G.inc_grid_cap = h->lc.coop_inc;
     G.inc_grid_mul = getenv("PGSI_INC_GRID_MUL") ? atoi(getenv("PGSI_INC_GRID_MUL")) : 16;
+    G.inc_fuse_e = getenv("PGSI_INC_FUSE_E") ? atoi(getenv("PGSI_INC_FUSE_E")) : 0;   // measured slower
+    G.inc_skip_v1 = getenv("PGSI_INC_SKIP_V1") ? atoi(getenv("PGSI_INC_SKIP_V1")) : 1;
     G.inc_max_steps = 1;
     // children CSR scratch of the BFS valuation (§V-bfs)
     CKL(dalloc(h, &G.ccnt, N1));

@@ -135,6 +135,9 @@ struct DevGame {
     int32_t inc_grid_cap;   // cooperative grid cap of k_inc_iter
     int32_t inc_grid_mul;   // k_inc_iter grid = |S| * inc_grid_mul threads (capped)
     int64_t inc_s_div;      // incremental step only while |S| * inc_s_div <= n'
+    int32_t inc_s_odd;      // the switch list S of the first incremental step came from All_Odd
+    int32_t inc_fuse_e;     // build E inside the dirty-closure scan (else a separate pass)
+    int32_t inc_skip_v1;    // after All_Odd steps replace V1 on D by the V2 walk depth
 };
 
 struct LaunchCfg {

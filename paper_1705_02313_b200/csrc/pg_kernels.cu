@@ -1102,6 +1102,11 @@ __device__ __forceinline__ void expand_rev(const DevGame &g, int32_t f, uint32_t
 // S (marked before the first level) can be met twice, so a plain mark load
 // replaces the atomic exchange. The child's own reverse range is loaded in the
 // same step as its succ and stored beside it (the next level starts at rcol).
+//
+// The same scan builds E (step 4 of k_inc_iter): every Odd game predecessor u of a
+// D vertex has a candidate in D, and every D vertex is expanded exactly once (the
+// last level included), so E = the Odd u met here, deduplicated by an atomic
+// exchange on its E mark issued with the batch's loads.
 __device__ __forceinline__ void expand_closure(const DevGame &g, int32_t f, uint32_t rb, uint32_t re,
                                                uint32_t ep, int32_t *outv, uint2 *outr,
                                                unsigned long long *cnt) {
@@ -1123,6 +1128,12 @@ __device__ __forceinline__ void expand_closure(const DevGame &g, int32_t f, uint
             mk[j] = __ldcg(g.dmark + x);
             ub[j] = __ldg(g.rrp + x);
             ue[j] = __ldg(g.rrp + x + 1);
+        }
+        if (g.inc_fuse_e) {
+            bool oe[8];
+#pragma unroll
+            for (int j = 0; j < 8; j++) oe[j] = u[j] >= 0 && u[j] >= g.n_even && atomicExch(g.emark + u[j], ep) != ep;
+            warp_append8(u, oe, g.El, &g.ctl->nE);
         }
 #pragma unroll
         for (int j = 0; j < 8; j++) ok[j] = u[j] >= 0 && su[j] == f && mk[j] != ep;
@@ -1219,10 +1230,21 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
     const int64_t nd = hi;
     trace_ts(g, 1);
     trace_ts(g, 2);
+    // S came from an All_Odd step (every step after the first of a launch, and the
+    // first when the host says so): then every vertex of D ends finite. Odd switches
+    // strictly improve for Odd: val'(s) ⊑ e_pri(s) + val(b) ⊏ val(s)
+    // for each switched s, and val' ⊑ val pointwise, so every s is finite afterwards,
+    // and the play of a dirty vertex reaches some s. V1 is then replaced by the V2
+    // walk: depth(v) = walk length + depth(x) at the first clean vertex x. (A walk
+    // ending at a clean ⊤ vertex would contradict this; it sets inc_overflow and the
+    // host redoes the step in full, so results never depend on the argument.)
+    const bool odd_s = (step > 0 || g.inc_s_odd) && g.inc_skip_v1;
+    unsigned long long *jl = g.jl;
+    int r = 0;
+    if (!odd_s) {
     // ---- 2. V1 on D (init), with C ∪= D (every vertex whose valuation may have
     // changed since the last All_Even). A vertex occurs once in D, so its C mark
     // is a plain load and store.
-    unsigned long long *jl = g.jl;
     for (int64_t b0 = wbase; b0 < nd; b0 += stride) {
         const int64_t i = b0 + lane;
         int32_t v = -1;
@@ -1235,7 +1257,6 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
         warp_append(addc, v, g.Cl, &ctl->nC);
     }
     gbar(ctl);
-    int r = 0;
     bool go = true;
     while (go && r < 64) {
         r++;
@@ -1268,18 +1289,29 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
         go = bcast_ld(&ctl->newfin[r % 3]) != 0;
         if (blockIdx.x == 0 && threadIdx.x == 0) ctl->newfin[(r + 2) % 3] = 0;
     }
+    }
 
-    // ---- 3. V2 on D
+    // ---- 3. V2 on D (after an All_Odd step also V1's depth, and the C marks)
     trace_ts(g, 3);
     uint8_t *hb = hsm[threadIdx.x];
     uint32_t *ow = osm[threadIdx.x];
 #pragma unroll
     for (int k = 0; k < 32; k++) hb[k] = 0;
     unsigned long long wsteps = 0;
-    for (int64_t i = tid; i < nd; i += stride) {
-        const int32_t v = __ldcg(g.Dl + i);
-        const unsigned long long e = __ldcg(jl + v);
-        const bool fin = (uint32_t)e == SINK;
+    for (int64_t b0 = wbase; b0 < nd; b0 += stride) {   // warp-uniform (warp_append)
+        const int64_t i = b0 + lane;
+        const int32_t v = i < nd ? __ldcg(g.Dl + i) : -1;
+        if (odd_s) {
+            const bool addc = v >= 0 && __ldcg(g.cmark + v) != g.cepoch;
+            if (addc) g.cmark[v] = g.cepoch;
+            warp_append(addc, v, g.Cl, &ctl->nC);
+        }
+        if (v < 0) continue;
+        bool fin = true;
+        if (!odd_s) {
+            const unsigned long long e = __ldcg(jl + v);
+            fin = (uint32_t)e == SINK;
+        }
         g.top[v] = fin ? 0 : 1;
         if (!fin) {
             put_cpx(g, v, make_uint4(1u, 0, 0, 0), make_uint4(0, 0, 0, 0));
@@ -1295,23 +1327,37 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
             steps++;
         }
         wsteps += steps;
+        if (odd_s) {   // depth(v) = steps + depth(x); x is clean (final jl) or the sink
+            uint32_t dx = 0;
+            if (x != (int32_t)N) {
+                const unsigned long long ex = __ldcg(jl + x);
+                if ((uint32_t)ex != SINK) atomicOr(&ctl->inc_overflow, 1ull);   // clean ⊤ exit: redo in full
+                dx = (uint32_t)(ex >> 32);
+            }
+            uint32_t dv = steps + dx;
+            if (dv > 0x7fffffffu) dv = 0x7fffffffu;
+            jl[v] = pack_jl(SINK, dv);
+        }
         cpx_merge_store(g, v, hb, mask, x, ow);
     }
     gbar(ctl);
 
-    // ---- 4. E = Odd vertices with a candidate in D
+    // ---- 4. E = Odd vertices with a candidate in D: built by the closure scan
+    // (inc_fuse_e) or by a pass over D's reverse edges
     trace_ts(g, 4);
-    for (int64_t b0 = wbase; b0 < nd; b0 += stride) {
-        const int64_t i = b0 + lane;
-        uint32_t rb = 0, re = 0;
-        if (i < nd) {
-            const uint2 r = __ldcg(g.Dr + i);
-            rb = r.x;
-            re = r.y;
+    if (!g.inc_fuse_e) {
+        for (int64_t b0 = wbase; b0 < nd; b0 += stride) {
+            const int64_t i = b0 + lane;
+            uint32_t rb = 0, re = 0;
+            if (i < nd) {
+                const uint2 rr = __ldcg(g.Dr + i);
+                rb = rr.x;
+                re = rr.y;
+            }
+            expand_rev<1>(g, -1, rb, re, g.emark, ep, g.El, &ctl->nE);
         }
-        expand_rev<1>(g, -1, rb, re, g.emark, ep, g.El, &ctl->nE);
+        gbar(ctl);
     }
-    gbar(ctl);
     const int64_t ne = (int64_t)bcast_ld(&ctl->nE);
     const bool ovf = bcast_ld(&ctl->inc_overflow) != 0;
     trace_ts(g, 5);
