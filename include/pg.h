@@ -155,6 +155,10 @@ typedef struct {
     double ms_dist;          /* host wall time inside the exchange callback                 */
     int64_t prefix_gathers;  /* 32 B prefix gathers of the switch steps after an undecided
                                 8 B switch-key compare (DESIGN.md §4 switch keys)          */
+    int64_t small_solves;    /* pg_solve calls run entirely by the single-block kernel
+                                (k_solve_small: its state, n'·(8·dp + 9) bytes, fits in
+                                shared memory; no PG_BELLMAN_FORD; not sharded):
+                                Algorithm 1 with no host round trip                    */
     /* PG_BELLMAN_FORD arm */
     int64_t bf_rounds;       /* relaxation rounds (= inner_iters of a BF solve)             */
     double ms_bf;            /* PG_PHASE_TIMING: CUDA-event total of the rounds             */

@@ -68,6 +68,9 @@ struct pg_game_s {
     int2 *swl_all = nullptr;          // world × max(|S_r|) gathered switch lists
     size_t swl_all_cap = 0;
     int64_t *h_x = nullptr;           // pinned scratch (exchange counts, total |S|)
+    // whole-solve single-block path for small games (pg_small.cu)
+    int64_t small_max = INT64_MAX;    // n' + 1 up to this (PGSI_SMALL_MAX; 0 disables)
+    int smem_optin = 0;               // max dynamic shared memory per block (bytes)
     // Bellman-Ford arm (PG_BELLMAN_FORD): double-buffered key rows (⊤ = all INT_MAX)
     int32_t *bf_row[2] = {nullptr, nullptr};
 };
@@ -854,6 +857,9 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     G.inc_s_div = h->inc_s_div;
     G.inc_grid_cap = h->lc.coop_inc;
     G.inc_grid_mul = getenv("PGSI_INC_GRID_MUL") ? atoi(getenv("PGSI_INC_GRID_MUL")) : 16;
+    if (getenv("PGSI_SMALL_MAX")) h->small_max = atoll(getenv("PGSI_SMALL_MAX"));
+    if (cudaDeviceGetAttribute(&h->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device) != cudaSuccess)
+        h->smem_optin = 48 * 1024;
     G.inc_fuse_e = getenv("PGSI_INC_FUSE_E") ? atoi(getenv("PGSI_INC_FUSE_E")) : 0;   // measured slower
     G.inc_skip_v1 = getenv("PGSI_INC_SKIP_V1") ? atoi(getenv("PGSI_INC_SKIP_V1")) : 1;
     G.inc_max_steps = 1;
@@ -1047,7 +1053,35 @@ pg_status pg_solve(pg_game h, uint8_t *winner, int32_t *sigma, int32_t *tau, int
             CK(h, launch_init_profile(h->G, h->stream));   // σ_init, τ = first successor
             h->st.gpu_launches += 1;
         }
-        for (;;) {                                           // Algorithm 1, outer repeat
+        // the whole of Algorithm 1 in one single-block launch (pg_small.cu) when its state
+        // fits in shared memory
+        const bool small = h->G.n_int + 1 <= h->small_max && !h->dist_fn && !(h->flags & PG_BELLMAN_FORD) &&
+                           small_scratch_bytes(h->G.n_int, h->G.dp, check) <= (size_t)h->smem_optin;
+        if (small) {
+            {
+                PhaseScope ps(h, PH_OTHER);
+                CK(h, launch_solve_small(h->G, check, (h->flags & PG_SI_RESET) != 0, h->max_inner, h->max_outer,
+                                         h->stream));
+                h->st.gpu_launches += 1;
+            }
+            if ((rc = readback(h))) return rc;
+            inner = (int64_t)h->h_ctl->sm_inner;
+            outer = (int64_t)h->h_ctl->sm_outer;
+            h->st.v1_rounds += (int64_t)h->h_ctl->v1_rounds;
+            h->st.odd_switches += (int64_t)h->h_ctl->odd_switches;
+            h->st.even_switches += (int64_t)h->h_ctl->even_switches;
+            h->st.small_solves++;
+            h->have_state = false;   // jl / prefixes do not describe the final profile
+            h->c_valid = false;
+            if (h->h_ctl->sm_status == 1) {
+                set_err(h->max_outer > 0 && outer >= h->max_outer ? "outer pass cap reached" : "inner iteration cap reached");
+                rc = PG_EITERCAP;
+            } else if (h->h_ctl->sm_status == 2) {
+                set_err("odd cycle reached: strategy not admissible");
+                rc = PG_EINADMISSIBLE;
+            }
+        }
+        for (; !small;) {                                    // Algorithm 1, outer repeat
             if (h->max_outer > 0 && outer >= h->max_outer) {
                 set_err("outer pass cap reached");
                 rc = PG_EITERCAP;

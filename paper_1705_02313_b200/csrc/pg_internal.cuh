@@ -71,6 +71,9 @@ struct Ctl {
     unsigned long long nC;          // |C|: vertices in some dirty set since the last All_Even
     unsigned long long bf_changed;  // Bellman-Ford round: vertices whose value changed
     unsigned long long bf_rows;     // ... finite rows gathered, compared or written
+    unsigned long long sm_inner;    // k_solve_small: inner iterations, outer passes, status
+    unsigned long long sm_outer;
+    unsigned long long sm_status;   // 0 ok, 1 iteration cap, 2 odd cycle
     unsigned int bar_count;         // grid barrier
     unsigned int bar_gen;
     unsigned long long ts[12];      // PGSI_TRACE=2: %globaltimer at the incremental kernel's phase ends
@@ -166,6 +169,10 @@ size_t children_scan_bytes(int64_t n1);
 // Bellman-Ford arm (pg_bf.cu): one synchronous relaxation round cur -> nxt
 cudaError_t launch_bf_round(const DevGame &g, int sms, const int32_t *cur, int32_t *nxt,
                             unsigned long long *changed, unsigned long long *rows, cudaStream_t s);
+// whole-solve single-block kernel for small games (pg_small.cu)
+size_t small_scratch_bytes(int64_t n_int, int dp, bool check);
+cudaError_t launch_solve_small(const DevGame &g, bool check, bool reset, int64_t max_inner, int64_t max_outer,
+                               cudaStream_t s);
 cudaError_t launch_bf_init(int32_t *rows0, int32_t *rows1, int64_t count, int sms, cudaStream_t s);
 cudaError_t launch_export_val(const DevGame &g, int64_t count, int32_t *val_out, uint8_t *top_out,
                               cudaStream_t s);

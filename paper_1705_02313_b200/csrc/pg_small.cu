@@ -1,0 +1,228 @@
+// pg_small.cu — the whole of Algorithm 1 in ONE thread-block
+// launch for small games: the inner Odd loop and the outer Even loop run on the
+// device with no host round trip (north_star: "the outer Even improvement loop,
+// kept entirely on device").
+//
+// For large games the host drives the loop with one readback per launch, which is
+// noise next to millisecond iterations. For small games (configs[0], the F_stair
+// long-iteration family) the round trips dominate: about 60-100 µs per iteration
+// against a few µs of work. Here one block of 1024 threads holds everything: full
+// d-vector key rows (k_i = sgn(D[i])·count_i, ⊑ = lexicographic from the top
+// column, stored column-major), pointer-jumping state and ⊤ flags, all in shared
+// memory. The host takes this path only when they fit (n' · (8·dp + 9) bytes within
+// the 227 KB opt-in limit): measured against the multi-kernel loop it is 2-5× faster
+// there, and slower as soon as the rows spill to L2. Every barrier
+// is a __syncthreads.
+//
+// Per inner iteration:
+//   valuation   Wyllie pointer jumping on (J, row) pairs, double-buffered: a round
+//               sets row'(v) = row(v) + row(J(v)) and J'(v) = J(J(v)) for
+//               unfinished v (PAPER.md:613-632 over d-vectors; §8(a4) design W). It
+//               stops after the first round in which no vertex newly reaches the sink
+//               (DESIGN.md §V1 rule). Unfinished vertices are ⊤. In check mode a
+//               max-combine pass gives each ⊤ vertex its cycle's dominant priority
+//               (PAPER.md:666-676); an odd one is PG_EINADMISSIBLE.
+//   All_Odd     per Odd vertex: the first ⊑-minimal candidate; switch iff strictly
+//               better than the current choice (readings 1-3, 5). The decision reads
+//               only rows and the vertex's own choice, so switches apply in place.
+//   convergence __syncthreads_count of the switches (Algorithm 1 "until").
+// Per outer pass, All_Even (greedy all-switches, sink candidate last). Results and
+// iteration counts are identical to the multi-kernel path; the GPU tests check both
+// against the oracle.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "pg_internal.cuh"
+
+namespace pgsi {
+
+constexpr int kSmallThreads = 1024;
+
+struct SmallLayout {   // offsets (bytes) inside one scratch region
+    size_t rows[2], J[2], top, M[2], MJ[2], total;
+};
+
+static SmallLayout small_layout(int64_t n1, int dp, bool check) {
+    SmallLayout L{};
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 15) & ~size_t(15); return o; };
+    for (int b = 0; b < 2; b++) L.rows[b] = take((size_t)n1 * dp * 4);
+    for (int b = 0; b < 2; b++) L.J[b] = take((size_t)n1 * 4);
+    L.top = take((size_t)n1);
+    for (int b = 0; b < 2; b++) { L.M[b] = check ? take((size_t)n1 * 4) : 0; L.MJ[b] = check ? take((size_t)n1 * 4) : 0; }
+    L.total = off;
+    return L;
+}
+
+size_t small_scratch_bytes(int64_t n_int, int dp, bool check) { return small_layout(n_int + 1, dp, check).total; }
+
+// a ⊏ b on (row, ⊤) pairs; the sink is the finite zero row. Rows are column-major
+// (column i of vertex v at rows[i·n1 + v]) so that the thread-per-vertex loops of a
+// warp touch consecutive words (coalesced in L1, conflict-free in shared memory).
+__device__ __forceinline__ bool sm_less(const int32_t *rows, const uint8_t *top, int dp, int32_t n1, int32_t sink,
+                                        int32_t a, int32_t b) {
+    const bool ta = a != sink && top[a], tb = b != sink && top[b];
+    if (ta) return false;
+    if (tb) return true;
+    for (int i = dp - 1; i >= 0; i--) {
+        const int32_t x = a == sink ? 0 : rows[(int64_t)i * n1 + a];
+        const int32_t y = b == sink ? 0 : rows[(int64_t)i * n1 + b];
+        if (x != y) return x < y;
+    }
+    return false;
+}
+
+__global__ void __launch_bounds__(kSmallThreads) k_solve_small(DevGame g, SmallLayout L, int check, int reset,
+                                                               int64_t max_inner, int64_t max_outer) {
+    extern __shared__ int4 smem4[];
+    char *base = reinterpret_cast<char *>(smem4);
+    int32_t *const rows0 = reinterpret_cast<int32_t *>(base + L.rows[0]);
+    int32_t *const rows1 = reinterpret_cast<int32_t *>(base + L.rows[1]);
+    int32_t *const J0 = reinterpret_cast<int32_t *>(base + L.J[0]);
+    int32_t *const J1 = reinterpret_cast<int32_t *>(base + L.J[1]);
+    uint8_t *top = reinterpret_cast<uint8_t *>(base + L.top);
+    const int32_t N = (int32_t)g.n_int, SINK = N, n1 = N + 1;
+    const int dp = g.dp;
+    const int t = threadIdx.x, T = blockDim.x;
+    int64_t inner = 0, outer = 0, rounds = 0, odd_sw = 0, even_sw = 0;
+    int status = 0;   // 0 ok, 1 iteration cap, 2 odd cycle
+    int cur = 0;      // buffer holding the final rows / J of the last valuation
+    for (;;) {                                                        // Algorithm 1, outer repeat
+        if (max_outer > 0 && outer >= max_outer) { status = 1; break; }
+        if (reset && outer > 0) {                                     // SI-Reset: τ := τ_init
+            for (int32_t v = (int32_t)g.n_even + t; v < N; v += T) g.succ[v] = g.col[g.rp[v]];
+            __syncthreads();
+        }
+        bool stop = false;
+        for (;;) {                                                    // inner repeat
+            if (max_inner > 0 && inner >= max_inner) { status = 1; stop = true; break; }
+            // ---- valuation: round 0 = (succ, e_pri)
+            for (int32_t v = t; v <= N; v += T) {
+                const int p = v < N ? g.pidx[v] : -1;
+                for (int i = 0; i < dp; i++) rows0[(int64_t)i * n1 + v] = i == p ? (g.oddp[p] ? -1 : 1) : 0;
+                J0[v] = v < N ? g.succ[v] : SINK;
+            }
+            __syncthreads();
+            int c = 0;
+            for (;;) {
+                int newly = 0;
+                const int32_t *Rc = c ? rows1 : rows0;
+                int32_t *Rn = c ? rows0 : rows1;
+                const int32_t *Jc = c ? J1 : J0;
+                int32_t *Jn = c ? J0 : J1;
+                for (int32_t v = t; v < N; v += T) {
+                    const int32_t w = Jc[v];
+                    if (w == SINK) {
+                        for (int i = 0; i < dp; i++) Rn[(int64_t)i * n1 + v] = Rc[(int64_t)i * n1 + v];
+                        Jn[v] = SINK;
+                    } else {
+                        for (int i = 0; i < dp; i++)
+                            Rn[(int64_t)i * n1 + v] = Rc[(int64_t)i * n1 + v] + Rc[(int64_t)i * n1 + w];
+                        const int32_t jw = Jc[w];
+                        Jn[v] = jw;
+                        newly += jw == SINK;
+                    }
+                }
+                if (t == 0) Jn[N] = SINK;
+                rounds++;
+                c ^= 1;
+                if (__syncthreads_count(newly) == 0) break;
+            }
+            cur = c;
+            {
+                const int32_t *Jf = cur ? J1 : J0;
+                for (int32_t v = t; v < N; v += T) top[v] = Jf[v] != SINK;
+            }
+            __syncthreads();
+            inner++;
+            if (check) {   // cycle-dominant priority of ⊤ vertices by max-combine jumping
+                int32_t *const M0 = reinterpret_cast<int32_t *>(base + L.M[0]);
+                int32_t *const M1 = reinterpret_cast<int32_t *>(base + L.M[1]);
+                int32_t *const MJ0 = reinterpret_cast<int32_t *>(base + L.MJ[0]);
+                int32_t *const MJ1 = reinterpret_cast<int32_t *>(base + L.MJ[1]);
+                for (int32_t v = t; v <= N; v += T) {
+                    M0[v] = v < N ? g.pidx[v] : 0;
+                    MJ0[v] = v < N ? g.succ[v] : SINK;
+                }
+                __syncthreads();
+                int b = 0;
+                for (int64_t span = 1; span < (int64_t)N + 1; span *= 2) {
+                    const int32_t *Mc = b ? M1 : M0, *MJc = b ? MJ1 : MJ0;
+                    int32_t *Mn = b ? M0 : M1, *MJn = b ? MJ0 : MJ1;
+                    for (int32_t v = t; v <= N; v += T) {
+                        const int32_t w = MJc[v];
+                        Mn[v] = max(Mc[v], Mc[w]);
+                        MJn[v] = MJc[w];
+                    }
+                    b ^= 1;
+                    __syncthreads();
+                }
+                const int32_t *Mf = b ? M1 : M0, *MJf = b ? MJ1 : MJ0;
+                int odd = 0;
+                for (int32_t v = t; v < N; v += T)
+                    if (top[v]) odd |= g.oddp[Mf[MJf[v]]];
+                if (__syncthreads_or(odd)) { status = 2; stop = true; break; }
+            }
+            // ---- All_Odd (in place: decisions read rows and the vertex's own choice)
+            const int32_t *R = cur ? rows1 : rows0;
+            int sw = 0;
+            for (int32_t v = (int32_t)g.n_even + t; v < N; v += T) {
+                const uint32_t e0 = g.rp[v], e1 = g.rp[v + 1];
+                int32_t best = g.col[e0];
+                for (uint32_t e = e0 + 1; e < e1; e++) {
+                    const int32_t u = g.col[e];
+                    if (sm_less(R, top, dp, n1, SINK, u, best)) best = u;
+                }
+                const int32_t cu = g.succ[v];
+                if (best != cu && sm_less(R, top, dp, n1, SINK, best, cu)) { g.succ[v] = best; sw++; }
+            }
+            const int nsw = __syncthreads_count(sw);
+            odd_sw += nsw;
+            if (nsw == 0) break;
+        }
+        if (stop) break;
+        outer++;
+        // ---- All_Even (greedy all-switches; the sink candidate is last)
+        const int32_t *R = cur ? rows1 : rows0;
+        int sw = 0;
+        for (int32_t v = t; v < (int32_t)g.n_even; v += T) {
+            const uint32_t e0 = g.rp[v], e1 = g.rp[v + 1];
+            int32_t best = g.col[e0];
+            for (uint32_t e = e0 + 1; e < e1; e++) {
+                const int32_t u = g.col[e];
+                if (sm_less(R, top, dp, n1, SINK, best, u)) best = u;
+            }
+            if (sm_less(R, top, dp, n1, SINK, best, SINK)) best = SINK;
+            const int32_t cu = g.succ[v];
+            if (best != cu && sm_less(R, top, dp, n1, SINK, cu, best)) { g.succ[v] = best; sw++; }
+        }
+        const int nsw = __syncthreads_count(sw);
+        even_sw += nsw;
+        if (nsw == 0) break;
+    }
+    for (int32_t v = t; v < N; v += T) g.top[v] = top[v];
+    if (t == 0) {
+        Ctl *ctl = g.ctl;
+        ctl->sm_inner = (unsigned long long)inner;
+        ctl->sm_outer = (unsigned long long)outer;
+        ctl->sm_status = (unsigned long long)status;
+        ctl->v1_rounds = (unsigned long long)rounds;
+        ctl->odd_switches = (unsigned long long)odd_sw;
+        ctl->even_switches = (unsigned long long)even_sw;
+    }
+}
+
+cudaError_t launch_solve_small(const DevGame &g, bool check, bool reset, int64_t max_inner, int64_t max_outer,
+                               cudaStream_t s) {
+    const SmallLayout L = small_layout(g.n_int + 1, g.dp, check);
+    if (L.total > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k_solve_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
+        if (e) return e;
+    }
+    k_solve_small<<<1, kSmallThreads, L.total, s>>>(g, L, check ? 1 : 0, reset ? 1 : 0, max_inner, max_outer);
+    return cudaGetLastError();
+}
+
+}  // namespace pgsi

@@ -65,7 +65,7 @@ class Stats(C.Structure):
         ("ms_inc", C.c_double),
         ("n_inc", C.c_int64), ("bytes_inc", C.c_double),
         ("dist_exchanges", C.c_int64), ("dist_bytes", C.c_int64), ("ms_dist", C.c_double),
-        ("prefix_gathers", C.c_int64),
+        ("prefix_gathers", C.c_int64), ("small_solves", C.c_int64),
         ("bf_rounds", C.c_int64), ("ms_bf", C.c_double), ("n_bf", C.c_int64), ("bytes_bf", C.c_double)]
 
     def as_dict(self):

@@ -13,6 +13,16 @@ from oracle import Oracle
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True, params=["auto", "multikernel"])
+def solve_path(request, monkeypatch):
+    """Every test runs twice: with the library's default dispatch (games with
+    n' + 1 <= 8192 solve in the single-block whole-solve kernel, k_solve_small) and
+    with that path disabled (PGSI_SMALL_MAX=0), so both paths meet the oracle."""
+    if request.param == "multikernel":
+        monkeypatch.setenv("PGSI_SMALL_MAX", "0")
+    return request.param
+
+
 @pytest.fixture(scope="module")
 def pg():
     import torch

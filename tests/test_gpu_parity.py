@@ -15,6 +15,16 @@ from oracle import Oracle, OracleError
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True, params=["auto", "multikernel"])
+def solve_path(request, monkeypatch):
+    """Every test runs twice: with the library's default dispatch (games with
+    n' + 1 <= 8192 solve in the single-block whole-solve kernel, k_solve_small) and
+    with that path disabled (PGSI_SMALL_MAX=0), so both paths meet the oracle."""
+    if request.param == "multikernel":
+        monkeypatch.setenv("PGSI_SMALL_MAX", "0")
+    return request.param
+
+
 @pytest.fixture(scope="module")
 def pg():
     import torch
@@ -375,7 +385,8 @@ def test_bfs_valuation_matches_pipeline(pg, n, d, seed):
     assert_solve_equal(rp, ora, n, rp.val.shape[1])
 
 
-def test_bfs_abort_on_deep_game(pg):
+def test_bfs_abort_on_deep_game(pg, monkeypatch):
+    monkeypatch.setenv("PGSI_SMALL_MAX", "0")   # the BFS valuation belongs to the multi-kernel path
     g = gi.f_deep(5000)
     ora = Oracle(g).solve()
     r = pg.Game.from_game(g, bfs=True).solve(want_val=True)
@@ -399,3 +410,30 @@ def test_inc_multi_step_launches(pg, monkeypatch):
     assert runs["1"]["n_inc"] >= runs["1"]["inc_valuations"]
     assert runs["1000000"]["inc_valuations"] > 0
     assert runs["1000000"]["n_inc"] < runs["1000000"]["inc_valuations"]
+
+
+def test_small_path_dispatch_caps_and_check(pg, solve_path):
+    """The single-block whole-solve kernel (k_solve_small) runs Algorithm 1 with no
+    host round trip: one launch per solve; caps and the odd-cycle check behave as
+    in the multi-kernel path."""
+    g = gi.random_game(1500, 6, 2, 5, 5)   # n' ≈ 2000, dp = 8: 146 KB of shared memory
+    ora = Oracle(g).solve()
+    G = pg.Game.from_game(g)
+    res = G.solve(want_val=True)
+    assert_solve_equal(res, ora, g.n, G.d)
+    assert res.stats["small_solves"] == (1 if solve_path == "auto" else 0)
+    big = gi.random_game(30000, 6, 2, 5, 5)   # does not fit: multi-kernel path
+    assert pg.Game.from_game(big).solve().stats["small_solves"] == 0
+    for kw in (dict(max_outer=1), dict(max_inner=3)):
+        with pytest.raises(pg.PGError) as e:
+            pg.Game.from_game(g, **kw).solve()
+        assert e.value.name == "PG_EITERCAP"
+    G = pg.Game.from_game(gi.from_adjacency([1, 1], [3, 1], [[1], [0]]), preprocess=False)
+    with pytest.raises(pg.PGError) as e:
+        G.solve()
+    assert e.value.name == "PG_EINADMISSIBLE"
+    # check mode on an admissible game and d > 32 rows
+    g = gi.random_game(200, 45, 1, 4, 9)
+    ora = Oracle(g).solve()
+    G = pg.Game.from_game(g, check=True)
+    assert_solve_equal(G.solve(want_val=True), ora, g.n, G.d)
