@@ -862,6 +862,7 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
         h->smem_optin = 48 * 1024;
     G.inc_fuse_e = getenv("PGSI_INC_FUSE_E") ? atoi(getenv("PGSI_INC_FUSE_E")) : 0;   // measured slower
     G.inc_skip_v1 = getenv("PGSI_INC_SKIP_V1") ? atoi(getenv("PGSI_INC_SKIP_V1")) : 1;
+    G.inc_blk_frontier = getenv("PGSI_INC_BLK") ? atoi(getenv("PGSI_INC_BLK")) : 256;
     G.inc_max_steps = 1;
     // children CSR scratch of the BFS valuation (§V-bfs)
     CKL(dalloc(h, &G.ccnt, N1));

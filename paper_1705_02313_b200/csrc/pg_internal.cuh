@@ -71,6 +71,7 @@ struct Ctl {
     unsigned long long nC;          // |C|: vertices in some dirty set since the last All_Even
     unsigned long long bf_changed;  // Bellman-Ford round: vertices whose value changed
     unsigned long long bf_rows;     // ... finite rows gathered, compared or written
+    unsigned long long blk[4];      // k_inc_iter thin-frontier closure in block 0: lo, hi, levels, abort
     unsigned long long sm_inner;    // k_solve_small: inner iterations, outer passes, status
     unsigned long long sm_outer;
     unsigned long long sm_status;   // 0 ok, 1 iteration cap, 2 odd cycle
@@ -141,6 +142,7 @@ struct DevGame {
     int32_t inc_s_odd;      // the switch list S of the first incremental step came from All_Odd
     int32_t inc_fuse_e;     // build E inside the dirty-closure scan (else a separate pass)
     int32_t inc_skip_v1;    // after All_Odd steps replace V1 on D by the V2 walk depth
+    int32_t inc_blk_frontier; // closure levels with at most this many frontier vertices run in block 0
 };
 
 struct LaunchCfg {

@@ -1202,6 +1202,52 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
     int64_t lo = 0, hi = ns;
     int levels = 0;
     while (lo < hi && levels < (1 << 30)) {
+        if (gridDim.x > 1 && hi - lo <= g.inc_blk_frontier) {
+            // Thin frontier (the long chains of a deep closure): block 0 runs the
+            // levels alone, separated by __syncthreads instead of a grid barrier plus
+            // a counter read, while the frontier stays thin; the grid resumes if it
+            // widens. Same expansion, same lists; only the synchronisation differs.
+            if (blockIdx.x == 0) {
+                __shared__ unsigned long long bcnt;
+                int64_t blo = lo, bhi = hi;
+                int blev = levels;
+                bool abort = false;
+                while (blo < bhi && bhi - blo <= 4 * (int64_t)g.inc_blk_frontier) {
+                    blev++;
+                    if (threadIdx.x == 0) bcnt = 0;
+                    __syncthreads();
+                    int32_t *out = g.Dl + bhi;
+                    for (int64_t b0 = blo + (threadIdx.x - lane); b0 < bhi; b0 += blockDim.x) {
+                        const int64_t i = b0 + lane;
+                        int32_t f = -1;
+                        uint2 r = make_uint2(0u, 0u);
+                        if (i < bhi) {
+                            f = __ldcg(g.Dl + i);
+                            r = __ldcg(g.Dr + i);
+                        }
+                        expand_closure(g, f, r.x, r.y, ep, out, g.Dr + bhi, &bcnt);
+                    }
+                    __syncthreads();
+                    blo = bhi;
+                    bhi += (int64_t)bcnt;
+                    if (blev >= g.inc_max_levels || bhi > g.inc_max_dirty) { abort = true; break; }
+                }
+                if (threadIdx.x == 0) {
+                    ctl->blk[0] = (unsigned long long)blo;
+                    ctl->blk[1] = (unsigned long long)bhi;
+                    ctl->blk[2] = (unsigned long long)blev;
+                    ctl->blk[3] = abort ? 1ull : 0ull;
+                    ctl->dcnt[0] = ctl->dcnt[1] = ctl->dcnt[2] = 0;
+                    if (abort) { ctl->inc_overflow = 1; ctl->nD = (unsigned long long)bhi; }
+                }
+            }
+            gbar(ctl);
+            lo = (int64_t)bcast_ld(&ctl->blk[0]);
+            hi = (int64_t)bcast_ld(&ctl->blk[1]);
+            levels = (int)bcast_ld(&ctl->blk[2]);
+            if (bcast_ld(&ctl->blk[3])) return;
+            continue;
+        }
         levels++;
         unsigned long long *cnt = &ctl->dcnt[levels % 3];   // reset two levels ahead: no block
         int32_t *out = g.Dl + hi;                           // reads a count still being written
