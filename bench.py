@@ -72,6 +72,32 @@ def ncu_traffic(kernel_prefix):
     return None, None
 
 
+def ncu_dram_summary(peak):
+    """north_star's HBM test from the committed ncu launch list of one
+    config-3 solve: actual DRAM bytes / duration per kernel (cold-cache, serialised
+    launches), and the time-weighted aggregates of the valuation kernels and of the
+    switch kernels. None if the profile is absent."""
+    path = os.path.join(ROOT, "profiles", "r1", "kernel_traffic.json")
+    try:
+        ks = json.load(open(path))["kernels"]
+    except (OSError, ValueError, KeyError):
+        return None
+    groups = {"valuation (k_v1, k_spl_*, k_v2_cpx, k_inc_iter)": ("k_v1", "k_spl_", "void k_spl_", "k_v2_cpx", "k_inc_iter"),
+              "odd switch (k_switch<1,*>)": ("void k_switch<1",),
+              "even switch (k_switch<0,*>, k_ebuild_even)": ("void k_switch<0", "k_ebuild_even"),
+              "bellman-ford round (k_bf_round)": ("void k_bf_round",)}
+    out = {"source": "profiles/r1/kernel_traffic.json", "peak_GBps": peak, "groups": {}}
+    for name, prefixes in groups.items():
+        b = t = 0.0
+        for k, v in ks.items():
+            if k.startswith(prefixes):
+                b += v["dram_bytes_per_launch"] * v["launches"]
+                t += v["ns_per_launch"] * v["launches"]
+        if t:
+            out["groups"][name] = {"dram_GBps": b / t, "frac_of_peak": b / t / peak}
+    return out
+
+
 def measured_peak_gbs():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -407,6 +433,7 @@ def main():
                        "l2": f"inputs larger than L2: per-iteration working set {ws_bytes / 1e9:.2f} GB "
                              f"(prefixes, jl, succ, pidx, ⊤, CSR) > 126 MB; no flush needed"},
             "roofline": roofline,
+            "hbm_actual": ncu_dram_summary(peak),
             "from_scratch": scratch,
             "arms": arms,
             "cpu_baseline": cpu,
