@@ -48,6 +48,8 @@ WORKLOADS = {
                   desc="Towers-of-Hanoi family k=13 (3.19M vertices, d=3; BASELINE configs[3])"),
     "elevator": dict(family="elevator", f=20, r=15, ref_iters=2, cpu_iters=4,
                      desc="elevator family (f=20, r=15): 1.97M vertices, d=3 (BASELINE configs[3])"),
+    "deep": dict(family="deep", L=4_000_000, ref_iters=1, cpu_iters=2,
+                 desc="F_deep(4M) closed-form family: one 4M-deep finite play, d=3 (BASELINE configs[3])"),
     "stair": dict(family="stair", L=5000, ref_iters=200, cpu_iters=400,
                   desc="F_stair(5000) long-iteration family: 5000 outer passes (BASELINE configs[4])"),
 }
@@ -167,6 +169,8 @@ def make_game(wl, seed):
         return gi.elevator(wl["f"], wl["r"], seed)
     if fam == "stair":
         return gi.f_stair(wl["L"])
+    if fam == "deep":
+        return gi.f_deep(wl["L"])
     return gi.random_game(wl["n"], wl["d"], wl["lo"], wl["hi"], seed)
 
 
