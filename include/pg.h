@@ -84,7 +84,9 @@ enum {
     PG_NO_INCREMENTAL = 16,   /* recompute every valuation from scratch (no dirty-closure
                                  incremental valuation; results are identical)          */
     PG_HOST_LOAD = 32,        /* run pg_load's transform on the host (pg_load.cpp) instead
-                                 of the GPU (pg_load_dev.cu); results are identical      */
+                                 of the GPU (pg_load_dev.cu); results are identical. Games
+                                 with n + m <= 32768 always load on the host, where it is
+                                 faster                                                  */
     PG_BFS = 64,              /* full valuations by top-down BFS over the functional forest
                                  (§V-bfs) instead of pointer jumping + walks; identical
                                  results, slower on B200 (scattered small writes)        */

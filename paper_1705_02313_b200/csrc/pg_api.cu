@@ -751,7 +751,12 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     // ---- §8(a1) load-time transform: on the GPU (default) or on the host
     DevLoadOut L;
     std::string err;
-    if (o.flags & PG_HOST_LOAD) {
+    // Tiny games: the host transform beats the device one, whose cost there is a
+    // dozen synchronising round trips (PGSI_HOST_LOAD_MAX = n + m limit; 0 = never).
+    int64_t host_max = 32768;
+    if (getenv("PGSI_HOST_LOAD_MAX")) host_max = atoll(getenv("PGSI_HOST_LOAD_MAX"));
+    const int64_t m_in = (n > 0 && row_ptr) ? row_ptr[n] : 0;
+    if ((o.flags & PG_HOST_LOAD) || n + m_in <= host_max) {
         HostGame H;
         pg_status rc = build_host_game(n, row_ptr, col, owner, priority, preprocess, H, err);
         if (rc) { set_err(err); return fail(rc); }

@@ -318,10 +318,11 @@ def test_best_response_large(pg):
 
 
 @pytest.mark.parametrize("seed", range(6))
-def test_device_load_matches_host_load(pg, seed):
+def test_device_load_matches_host_load(pg, seed, monkeypatch):
     """§8(a1) on the GPU (pg_load_dev.cu) vs the host transform (PG_HOST_LOAD):
     same internal game, hence identical valuations of the same ABI profile and
     identical solves (tie-breaks depend on the canonical adjacency order)."""
+    monkeypatch.setenv("PGSI_HOST_LOAD_MAX", "0")   # the GPU transform even for tiny games
     rng = np.random.default_rng(400 + seed)
     n = int(rng.integers(1, 30000))
     g = gi.random_game(n, int(rng.integers(1, 40)), 1, int(rng.integers(1, 7)), seed)
@@ -341,7 +342,8 @@ def test_device_load_matches_host_load(pg, seed):
     assert rd.stats["inner_iters"] == rh.stats["inner_iters"]
 
 
-def test_device_load_structured_and_duplicates(pg):
+def test_device_load_structured_and_duplicates(pg, monkeypatch):
+    monkeypatch.setenv("PGSI_HOST_LOAD_MAX", "0")
     for g in (gi.ladder(20000, 4), gi.hanoi(7), gi.f_deep(3000), gi.f_oddchain(500),
               gi.from_adjacency([1, 1, 0, 1], [5, 0, 2, 3], [[2, 1, 1, 0, 3, 3], [0, 1], [2, 2], [3]])):
         ora = Oracle(g).solve()
@@ -350,7 +352,8 @@ def test_device_load_structured_and_duplicates(pg):
 
 
 @pytest.mark.parametrize("bad", ["terminal", "range", "owner", "priority"])
-def test_device_load_errors_match_host(pg, bad):
+def test_device_load_errors_match_host(pg, bad, monkeypatch):
+    monkeypatch.setenv("PGSI_HOST_LOAD_MAX", "0")
     g = gi.random_game(200, 4, 1, 3, 9)
     if bad == "terminal":
         adj = [g.successors(v) for v in range(g.n)]
