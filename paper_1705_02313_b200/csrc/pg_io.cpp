@@ -158,28 +158,31 @@ bool parse(const char *text, int64_t len, Parsed &out, std::string &err) {
     return true;
 }
 
-// Tarjan's SCC algorithm, iterative. Vertex set: in[v]; edges: succ list per
-// vertex via the callback-free CSR (eb, ee, ecol). Returns a vertex x with
-// pri(x) == p lying on a cycle of the subgraph, or -1.
-int64_t cycle_through(int64_t n, const std::vector<uint8_t> &in, const std::vector<int64_t> &rp,
-                      const std::vector<int32_t> &adj, const int32_t *pri, int64_t p) {
-    std::vector<int64_t> index((size_t)n, -1), low((size_t)n, 0);
-    std::vector<uint8_t> onst((size_t)n, 0);
+// Tarjan's SCC algorithm, iterative, over the vertices `verts` (those of the
+// player's winning set with priority <= p) of the one-player graph (rp, adj); an
+// edge is followed iff its head is in the set (ok(w)). Buffers are reused across
+// calls: index[] must be -1 on entry for every vertex and is reset on exit.
+// Returns a vertex x with pri(x) == p lying on a cycle, or -1.
+template <typename InSet>
+int64_t cycle_through(const std::vector<int64_t> &verts, const std::vector<int64_t> &rp,
+                      const std::vector<int32_t> &adj, const int32_t *pri, int64_t p, InSet ok,
+                      std::vector<int64_t> &index, std::vector<int64_t> &low, std::vector<uint8_t> &onst) {
     std::vector<int64_t> st, cs, ce;   // SCC stack; call stack (vertex, next edge)
-    int64_t idx = 0;
-    for (int64_t s = 0; s < n; s++) {
-        if (!in[(size_t)s] || index[(size_t)s] >= 0) continue;
+    int64_t idx = 0, hit = -1;
+    for (int64_t s : verts) {
+        if (hit >= 0) break;
+        if (index[(size_t)s] >= 0) continue;
         cs.push_back(s);
         ce.push_back(rp[(size_t)s]);
         index[(size_t)s] = low[(size_t)s] = idx++;
         st.push_back(s);
         onst[(size_t)s] = 1;
-        while (!cs.empty()) {
+        while (!cs.empty() && hit < 0) {
             const int64_t v = cs.back();
             int64_t &e = ce.back();
             if (e < rp[(size_t)v + 1]) {
                 const int64_t w = adj[(size_t)e++];
-                if (!in[(size_t)w]) continue;
+                if (!ok(w)) continue;
                 if (index[(size_t)w] < 0) {
                     index[(size_t)w] = low[(size_t)w] = idx++;
                     st.push_back(w);
@@ -196,11 +199,10 @@ int64_t cycle_through(int64_t n, const std::vector<uint8_t> &in, const std::vect
             if (!cs.empty()) low[(size_t)cs.back()] = std::min(low[(size_t)cs.back()], low[(size_t)v]);
             if (low[(size_t)v] != index[(size_t)v]) continue;
             // v is the root of an SCC: pop it; a cycle exists if |SCC| > 1 or a self-loop
-            size_t top = st.size();
+            const size_t top = st.size();
             size_t pos = top;
             do { pos--; } while (st[pos] != v);
             const bool big = top - pos > 1;
-            int64_t hit = -1;
             for (size_t k = pos; k < top; k++) {
                 const int64_t x = st[k];
                 onst[(size_t)x] = 0;
@@ -211,10 +213,10 @@ int64_t cycle_through(int64_t n, const std::vector<uint8_t> &in, const std::vect
                 if (cyc) hit = x;
             }
             st.resize(pos);
-            if (hit >= 0) return hit;
         }
     }
-    return -1;
+    for (int64_t s : verts) { index[(size_t)s] = -1; onst[(size_t)s] = 0; }
+    return hit;
 }
 
 }  // namespace
@@ -291,26 +293,31 @@ pg_status pg_verify_solution(int64_t n, const int64_t *row_ptr, const int32_t *c
     std::vector<int32_t> ps(priority, priority + n);
     std::sort(ps.begin(), ps.end());
     ps.erase(std::unique(ps.begin(), ps.end()), ps.end());
+    std::vector<int64_t> index((size_t)n, -1), low((size_t)n, 0);
+    std::vector<uint8_t> onst((size_t)n, 0);
     for (int i = 0; i < 2; i++) {
         std::vector<int64_t> rp((size_t)n + 1, 0);
         std::vector<int32_t> adj;
+        std::vector<int64_t> order;   // W_i by ascending priority: H_p is a prefix
         for (int64_t v = 0; v < n; v++) {
             if (winner[v] == i) {
+                order.push_back(v);
                 if (owner[v] == i) adj.push_back(i == 0 ? sigma[v] : tau[v]);
                 else for (int64_t e = row_ptr[v]; e < row_ptr[v + 1]; e++) adj.push_back(col[e]);
             }
             rp[(size_t)v + 1] = (int64_t)adj.size();
         }
+        std::stable_sort(order.begin(), order.end(),
+                         [&](int64_t a, int64_t b) { return priority[a] < priority[b]; });
+        size_t end = 0;
+        std::vector<int64_t> verts;
         for (int32_t p : ps) {
+            while (end < order.size() && priority[order[end]] <= p) end++;
             if ((p & 1) == i) continue;   // only priorities good for the opponent
-            std::vector<uint8_t> in((size_t)n);
-            bool any = false;
-            for (int64_t v = 0; v < n; v++) {
-                in[(size_t)v] = winner[v] == i && priority[v] <= p;
-                any |= in[(size_t)v] && priority[v] == p;
-            }
-            if (!any) continue;
-            const int64_t x = cycle_through(n, in, rp, adj, priority, p);
+            if (end == 0 || priority[order[end - 1]] != p) continue;   // no p-vertex in W_i
+            verts.assign(order.begin(), order.begin() + (int64_t)end);
+            auto ok = [&](int64_t w) { return winner[w] == i && priority[w] <= p; };
+            const int64_t x = cycle_through(verts, rp, adj, priority, p, ok, index, low, onst);
             if (x >= 0)
                 return bad(x, std::string("a cycle with maximum priority ") + std::to_string(p) +
                                   " lies in the claimed winning set of " + (i == 0 ? "Even" : "Odd"));
