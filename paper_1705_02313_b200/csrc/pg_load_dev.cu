@@ -119,8 +119,27 @@ __global__ void kl_needs(int64_t n, const int64_t *cp, const int32_t *cc, const 
     }
 }
 
-__global__ void kl_present(int64_t n, const int32_t *pri, uint32_t *present) {
-    GS_LOOP(v, n) present[pri[v]] = 1;
+// Presence of each priority value. Few distinct values (d <= 256) hit by n stores
+// serialise on a handful of L2 lines, so each block first collects a bitmap in
+// shared memory (values < kPresBits) and ORs its nonzero words out once.
+constexpr int kPresBits = 1 << 15;
+__global__ void kl_present(int64_t n, const int32_t *pri, uint32_t *present, int32_t pmax) {
+    __shared__ uint32_t bm[kPresBits / 32];
+    const bool small = pmax < kPresBits;
+    const int words = small ? pmax / 32 + 1 : 0;
+    for (int w = threadIdx.x; w < words; w += blockDim.x) bm[w] = 0;
+    __syncthreads();
+    GS_LOOP(v, n) {
+        const int32_t p = pri[v];
+        if (small) atomicOr(&bm[p >> 5], 1u << (p & 31));
+        else present[p] = 1;
+    }
+    __syncthreads();
+    for (int w = threadIdx.x; w < words; w += blockDim.x)
+        for (uint32_t b = bm[w]; b; b &= b - 1) {
+            const int p = w * 32 + __ffs(b) - 1;
+            if (__ldcg(present + p) == 0) present[p] = 1;
+        }
 }
 
 __global__ void kl_iseven(int64_t n, const uint8_t *owner, uint32_t *ie) {
@@ -128,7 +147,16 @@ __global__ void kl_iseven(int64_t n, const uint8_t *owner, uint32_t *ie) {
 }
 
 __global__ void kl_pmax(int64_t n, const int32_t *pri, int32_t *pmax) {
-    GS_LOOP(v, n) atomicMax(pmax, pri[v]);
+    int32_t m = 0;   // priorities are validated >= 0
+    GS_LOOP(v, n) m = max(m, pri[v]);
+    for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    __shared__ int32_t red[32];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {   // one atomic per block instead of one per vertex
+        for (int w = 1; w < (int)(blockDim.x >> 5); w++) m = max(m, red[w]);
+        atomicMax(pmax, m);
+    }
 }
 
 __global__ void kl_collect_D(int32_t np1, const uint32_t *present, const uint32_t *pscan, int32_t *Dv) {
@@ -365,7 +393,7 @@ pg_status build_device_game(int64_t n, const int64_t *row_ptr, const int32_t *co
     CKD(sc.get(&d_pscan, (size_t)pmax + 2));
     CKD(sc.get(&d_Dv, (size_t)pmax + 2));
     CKD(cudaMemsetAsync(d_present, 0, 4 * ((size_t)pmax + 2), s));
-    if (n) kl_present<<<grid1(n), T, 0, s>>>(n, d_pri, d_present);
+    if (n) kl_present<<<grid1(n), T, 0, s>>>(n, d_pri, d_present, pmax);
     if (dummies) CKD(cudaMemsetAsync(d_present, 0x01, 1, s));   // priority 0 (little-endian word = 1)
     CKD(exscan(d_present, d_pscan, (int64_t)pmax + 2, s));
     uint32_t d = 0;
