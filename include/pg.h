@@ -313,6 +313,23 @@ pg_status pg_verify_solution(int64_t n, const int64_t *row_ptr, const int32_t *c
                              const int32_t *priority, const uint8_t *winner, const int32_t *sigma,
                              const int32_t *tau, int64_t *witness);
 
+/* pg_verify_solution_device: the same verdict as pg_verify_solution, computed on
+ * GPU `device`. (a) Closure is one kernel pass. (b) Parity is a
+ * negative-cycle test in the ⊑ order. Sign the priority
+ * counts against the player being checked; then a cycle is ⊑-negative iff its maximum
+ * priority has the opponent's parity. Synchronous Bellman-Ford rounds on the
+ * one-player graph of each winning set, with an escape edge to a sink from every
+ * vertex, reach a fixpoint iff no such cycle exists. A cycle in the argmin pointers,
+ * checked every 32 rounds, proves one. Host pointers as pg_verify_solution; d <= 32.
+ *   witness      int64* or NULL: an offending vertex (-1 if valid or unknown)
+ *   rounds       int64* or NULL: Bellman-Ford rounds run (both players)
+ * Returns PG_OK if the solution is correct, PG_EINVAL if not, PG_ENOTSUP for
+ * d > 32, PG_ECUDA on a CUDA error. */
+pg_status pg_verify_solution_device(int64_t n, const int64_t *row_ptr, const int32_t *col,
+                                    const uint8_t *owner, const int32_t *priority, const uint8_t *winner,
+                                    const int32_t *sigma, const int32_t *tau, int32_t device,
+                                    int64_t *witness, int64_t *rounds);
+
 /* pg_get_stats: statistics of the last call on the handle (host pointer). */
 pg_status pg_get_stats(pg_game g, pg_stats *stats);
 

@@ -101,7 +101,8 @@ def load_library(path: str = LIB_PATH):
     L.pg_parse_pgsolver.argtypes = [C.c_char_p, C.c_int64, P, P, P, P, P, P]
     L.pg_format_solution.argtypes = [C.c_int64, P, P, P, P, C.c_char_p, C.c_int64, P]
     L.pg_verify_solution.argtypes = [C.c_int64, P, P, P, P, P, P, P, P]
-    for f in ("pg_parse_pgsolver", "pg_format_solution", "pg_verify_solution"):
+    L.pg_verify_solution_device.argtypes = [C.c_int64, P, P, P, P, P, P, P, C.c_int32, P, P]
+    for f in ("pg_parse_pgsolver", "pg_format_solution", "pg_verify_solution", "pg_verify_solution_device"):
         getattr(L, f).restype = C.c_int
     L.pg_free.argtypes = [C.c_void_p]
     L.pg_free.restype = None
@@ -335,15 +336,21 @@ def format_solution(owner, winner, sigma, tau) -> str:
     return buf.value.decode()
 
 
-def verify_solution(g, winner, sigma, tau):
-    """(ok, witness, message) from ``pg_verify_solution`` on the original game g."""
+def verify_solution(g, winner, sigma, tau, device=None):
+    """(ok, witness, message) from ``pg_verify_solution`` on the original game g
+    (host C++), or from ``pg_verify_solution_device`` on GPU ``device``."""
     L = load_library()
     arrs = [np.ascontiguousarray(g.row_ptr, np.int64), np.ascontiguousarray(g.col, np.int32),
             np.ascontiguousarray(g.owner, np.uint8), np.ascontiguousarray(g.priority, np.int32),
             np.ascontiguousarray(winner, np.uint8), np.ascontiguousarray(sigma, np.int32),
             np.ascontiguousarray(tau, np.int32)]
     w = C.c_int64()
-    rc = L.pg_verify_solution(int(g.n), *[_ptr(a) for a in arrs], C.byref(w))
+    if device is not None:
+        rounds = C.c_int64()
+        rc = L.pg_verify_solution_device(int(g.n), *[_ptr(a) for a in arrs], int(device), C.byref(w),
+                                         C.byref(rounds))
+    else:
+        rc = L.pg_verify_solution(int(g.n), *[_ptr(a) for a in arrs], C.byref(w))
     if rc == 0:
         return True, -1, ""
     if rc != -1:

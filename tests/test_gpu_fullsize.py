@@ -4,8 +4,9 @@ configuration bench.py times (device pointers on torch's current stream, phase
 timing on). The oracle cannot solve this size in test time, so the checks are
 properties that hold at any size, each derived from the paper's definitions:
 
-- the solution verifies (pg_verify_solution: closure + per-priority cycle check,
-  PAPER.md:288-312), which pins the winning partition, since W is unique (Thm 1);
+- the solution verifies, on the host (pg_verify_solution: closure + per-priority
+  cycle check) and on the GPU (pg_verify_solution_device: closure + ⊑-negative-cycle
+  test) (PAPER.md:288-312). This pins the winning partition, since W is unique (Thm 1);
 - the three best-response arms agree on W, σ* and the outer passes (val^σ is
   unique, PAPER.md:392-394);
 - sampled vertices satisfy the valuation's defining recurrence
@@ -68,6 +69,8 @@ def test_config3_fullsize_bench_configuration(pg, cfg3):
     S = res.sigma.cpu().numpy()
     T = res.tau.cpu().numpy()
     ok, _, msg = pg.verify_solution(g, W, S, T)
+    assert ok, msg
+    ok, _, msg = pg.verify_solution(g, W, S, T, device=0)   # the GPU verifier agrees
     assert ok, msg
 
     # arms: same W, σ*, outer passes
