@@ -125,6 +125,21 @@ def test_sharded_solve_threads(pg, name, world):
     assert ag.calls >= ora.inner_iters
 
 
+@pytest.mark.parametrize("arm", ["si_reset", "bf"])
+def test_sharded_solve_arms(pg, arm):
+    """The best-response arms of Table 2 with sharded switch steps: SI-Reset
+    exchanges after every switch step, Bellman-Ford (replicated rounds, no All_Odd)
+    only after each All_Even."""
+    for g in (gi.random_game(6000, 10, 2, 5, 13), gi.ladder(8000, 2)):
+        ora = Oracle(g).solve(mode=arm)
+        hs, _ = sharded_handles(pg, g, 2, best_response=arm)
+        res = run_threads([lambda h=h: h.solve(want_val=True) for h in hs])
+        for r in res:
+            assert_solve_equal(r, ora, g.n, hs[0].d)
+            exp = ora.outer_passes + (ora.inner_iters if arm == "si_reset" else 0)
+            assert r.stats["dist_exchanges"] == exp
+
+
 @pytest.mark.parametrize("incremental", [True, False])
 def test_sharded_solve_modes(pg, incremental):
     """From-scratch switch steps (range mode) and check mode, world = 4 (some
