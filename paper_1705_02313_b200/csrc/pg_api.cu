@@ -57,7 +57,8 @@ struct pg_game_s {
     uint32_t epoch = 0;
     bool trace = false;               // PGSI_TRACE=1 (debug)
     bool c_valid = false;             // C covers every change since the last All_Even
-    int64_t inc_s_div = 16;           // incremental step when |S| * inc_s_div <= n'
+    int64_t inc_s_div = 16;           // incremental step when |S| * inc_s_div <= n' (S from All_Odd)
+    int64_t inc_s_div_even = 64;      // ... when S came from All_Even (V1 on D runs there)
     int64_t inc_max_steps = 1 << 20;  // inner iterations per incremental launch (PGSI_INC_STEPS)
     int64_t last_maxdepth = 0;        // deepest play of the last full valuation
     uint32_t cepoch = 0;
@@ -372,7 +373,8 @@ pg_status dist_exchange(pg_game h, bool odd) {
 // Incremental valuation pays off when the last switch step changed few choices.
 bool use_inc(pg_game h) {
     return h->have_state && h->G.dp <= 32 && h->last_nsw > 0 && !(h->flags & PG_NO_INCREMENTAL) &&
-           !(h->flags & PG_CHECK_INVARIANTS) && h->last_nsw * h->inc_s_div <= h->G.n_int;
+           !(h->flags & PG_CHECK_INVARIANTS) &&
+           h->last_nsw * (h->last_sw_odd ? h->inc_s_div : h->inc_s_div_even) <= h->G.n_int;
 }
 
 // Result of valuate_and_switch: valuations computed and the switches of the last
@@ -858,6 +860,7 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     G.bfs_max_levels = getenv("PGSI_BFS_MAX_LEVELS") ? atoi(getenv("PGSI_BFS_MAX_LEVELS")) : 160;
     G.inc_max_dirty = std::max<int64_t>(4096, L.n_int / (getenv("PGSI_INC_DIRTY_DIV") ? atoi(getenv("PGSI_INC_DIRTY_DIV")) : 8));
     h->inc_s_div = getenv("PGSI_INC_S_DIV") ? atoi(getenv("PGSI_INC_S_DIV")) : 16;
+    h->inc_s_div_even = getenv("PGSI_INC_S_DIV_EVEN") ? atoi(getenv("PGSI_INC_S_DIV_EVEN")) : 64;
     h->inc_max_steps = getenv("PGSI_INC_STEPS") ? std::max(1, atoi(getenv("PGSI_INC_STEPS"))) : (1 << 20);
     G.inc_s_div = h->inc_s_div;
     G.inc_grid_cap = h->lc.coop_inc;
