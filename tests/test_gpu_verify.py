@@ -75,3 +75,21 @@ def test_device_verifier_structured_and_witness(pg):
     ok, w, msg = pg.verify_solution(g, np.ones(3, np.uint8), np.array([1, -2, 1], np.int32),
                                     np.array([-2, 0, -2], np.int32), device=0)
     assert not ok and w in (0, 1, 2) and "cycle" in msg
+
+
+def test_cli_solve_pgsolver_file(pg, tmp_path):
+    """python -m paper_1705_02313_b200 solve: PGSolver in, paritysol out, verified;
+    the solution equals the oracle's."""
+    import subprocess
+    import sys
+    g = gi.random_game(2000, 8, 1, 4, 17)
+    src = tmp_path / "g.pg"
+    src.write_text(gi.pgsolver_text(g))
+    out = tmp_path / "g.sol"
+    root = __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__)))
+    for verify in ("host", "gpu"):
+        p = subprocess.run([sys.executable, "-m", "paper_1705_02313_b200", "solve", str(src), "-o", str(out),
+                            "--verify", verify, "--stats"], cwd=root, capture_output=True, text=True, timeout=300)
+        assert p.returncode == 0, p.stderr
+    r = Oracle(g).solve()
+    assert out.read_text() == pg.format_solution(g.owner, r.winner, r.sigma, r.tau)
