@@ -825,6 +825,7 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     G.oddp = oddp;
     CKL(dalloc(h, &G.succ, N1));
     CKL(dalloc(h, &G.jl, N1));
+    CKL(dalloc(h, &G.s2p, N1));
     CKL(dalloc(h, &G.top, N1));
     CKL(dalloc(h, &G.cpx, N1 * 8));
     CKL(dalloc(h, &G.key, N1));

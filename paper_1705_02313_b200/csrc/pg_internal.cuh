@@ -95,6 +95,7 @@ struct DevGame {
     const uint8_t *oddp; // oddp[i] = D[i] is odd (dp entries, padding = 0)
     int32_t *succ;
     unsigned long long *jl;
+    unsigned long long *s2p;   // V1 round 1: succ(succ(v)) | pidx(v) << 32 | pidx(succ(v)) << 40
     uint8_t *top;
     int32_t *val;
     uint32_t *cpx;      // compact prefixes, 8 words per vertex (+ sink row of zeros)

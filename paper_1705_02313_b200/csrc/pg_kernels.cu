@@ -140,14 +140,20 @@ __global__ void __launch_bounds__(kThreads) k_v1(DevGame g) {
     unsigned long long *jl = g.jl;
     unsigned long long mx = 0, nf = 0, act = 0;
     // round 1 fused with init: J(v) = succ(succ(v)), len 2 (or the sink, len 1)
+    // The 2-step pointer is also kept with the two priorities it skips
+    // (s2p = s2 | pidx(v) << 32 | pidx(s1) << 40): V2's walks then take two steps
+    // per dependent load (k_v2_cpx). Only read by the V2 of the same valuation.
     for (int64_t v = tid; v < N; v += stride) {
         const uint32_t s1 = (uint32_t)__ldg(g.succ + v);
+        const unsigned long long p0 = (unsigned long long)__ldg(g.pidx + v) << 32;
         if (s1 == SINK) {
             jl[v] = pack_jl(SINK, 1u);
+            g.s2p[v] = (unsigned long long)SINK | p0;
             mx = mx > 1 ? mx : 1;
         } else {
             const uint32_t s2 = (uint32_t)__ldg(g.succ + s1);
             jl[v] = pack_jl(s2, 2u);
+            g.s2p[v] = (unsigned long long)s2 | p0 | ((unsigned long long)__ldg(g.pidx + s1) << 40);
             if (s2 == SINK) { mx = mx > 2 ? mx : 2; nf++; }
             else act++;
         }
@@ -515,7 +521,16 @@ __global__ void __launch_bounds__(kThreads) k_v2_cpx(DevGame g) {
         const uint32_t steps = depth < K ? depth : depth % K;
         uint32_t mask = 0;
         int32_t x = (int32_t)v;
-        for (uint32_t st = 0; st < steps; st++) {
+        uint32_t st = 0;
+        for (; st + 2 <= steps; st += 2) {   // two steps per dependent load (V1's s2p)
+            const unsigned long long w = __ldg(g.s2p + x);
+            const uint32_t p1 = (uint32_t)(w >> 32) & 0xffu, p2 = (uint32_t)(w >> 40) & 0xffu;
+            x = (int32_t)(uint32_t)w;
+            hb[p1]++;
+            hb[p2]++;
+            mask |= (1u << p1) | (1u << p2);
+        }
+        if (st < steps) {
             const uint32_t p = __ldg(g.pidx + x);
             x = __ldg(g.succ + x);
             hb[p]++;
