@@ -86,6 +86,8 @@ bool parse(const char *text, int64_t len, Parsed &out, std::string &err) {
     p.ws();
     if (p.word("parity")) {
         if (!p.num(maxid)) { err = p.err; return false; }
+        if (maxid >= (int64_t)INT32_MAX - 1) { p.fail("maxid too large"); err = p.err; return false; }
+        vs.reserve((size_t)maxid + 1);
         p.ws();
         if (!p.word(";")) { p.fail("expected ';' after the parity header"); err = p.err; return false; }
     }
@@ -104,6 +106,7 @@ bool parse(const char *text, int64_t len, Parsed &out, std::string &err) {
         if (ow > 1) { p.fail("owner must be 0 (Even) or 1 (Odd)"); err = p.err; return false; }
         if (pr > INT32_MAX) { p.fail("priority too large"); err = p.err; return false; }
         if (maxid >= 0 && id > maxid) { p.fail("vertex id " + std::to_string(id) + " exceeds the header's maxid"); err = p.err; return false; }
+        if (id >= (int64_t)INT32_MAX - 1) { p.fail("vertex id " + std::to_string(id) + " too large"); err = p.err; return false; }
         V &v = get(id);
         if (v.seen) { p.fail("duplicate definition of vertex " + std::to_string(id)); err = p.err; return false; }
         v.seen = true;

@@ -47,6 +47,7 @@ def test_parse_names_start_and_order(pg):
     ("parity 1;\n0 2 0 1\n1 1 1 0;", "expected ';'"),
     ("parity 1;\n0 2 0 1;\n1 x 1 0;", "line 3"),
     ("parity 0;\n3 2 0 1;", "exceeds"),
+    ("99999999999 2 0 1;", "too large"),
 ])
 def test_parse_errors(pg, txt, what):
     with pytest.raises(pg.PGError) as e:
