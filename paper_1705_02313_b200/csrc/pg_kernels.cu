@@ -127,10 +127,11 @@ __global__ void k_import_strategy(DevGame g, const int32_t *abi, int mode) {
 // --------------------------------------------------------------------------
 // V1: sink reachability, ⊤ detection and depth by pointer jumping on packed
 // (J, len) words. Round 1 is fused with the
-// initialisation (J = succ∘succ, synchronous); later rounds jump in place over a
-// compacted list of still-unfinished vertices. Stop after the first round in
-// which no vertex newly reaches the sink (exact); the vertices
-// left on the list are exactly the ⊤ vertices.
+// initialisation (J = succ∘succ, synchronous); later rounds jump in place over
+// all vertices in vertex order, skipping finished words (a compacted list of
+// unfinished vertices measured 2.3× slower: DESIGN.md negative results). Stop
+// after the first round in which no vertex newly reaches the sink (DESIGN.md §V1:
+// exact); the vertices still unfinished then are exactly the ⊤ vertices.
 // --------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads) k_v1(DevGame g) {
     const int64_t N = g.n_int;
