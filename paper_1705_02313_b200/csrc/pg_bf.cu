@@ -156,7 +156,8 @@ __global__ void __launch_bounds__(kThreads) k_bf_round(DevGame g, const int32_t 
 #pragma unroll
             for (int b = 0; b < B; b++) {
                 if (c0 + b >= maxc) break;                  // warp-uniform
-                const int cmp = row_cmp<G, C, W>(r[b], best, gb, gmask);
+                // the first candidate is taken unconditionally: no compare needed
+                const int cmp = (c0 == 0 && b == 0) ? -1 : row_cmp<G, C, W>(r[b], best, gb, gmask);
                 if (u[b] >= 0) {
                     // strict improvement only: the first ⊑-minimal candidate wins (reading 3)
                     if (barg < 0 || cmp < 0) {
@@ -183,7 +184,12 @@ __global__ void __launch_bounds__(kThreads) k_bf_round(DevGame g, const int32_t 
                         if (k == q / G && w == p % W) best[k][w] += inc;
             }
         }
-        const int dcmp = row_cmp<G, C, W>(best, old, gb, gmask);
+        bool ne = false;   // changed? (equality only: one ballot, no order)
+#pragma unroll
+        for (int k = 0; k < C; k++)
+#pragma unroll
+            for (int w = 0; w < W; w++) ne |= best[k][w] != old[k][w];
+        const int dcmp = ((__ballot_sync(FULLM, ne) >> gb) & gmask) != 0;
         if (act) {
             if (!btop) {
 #pragma unroll
