@@ -869,6 +869,7 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     if (getenv("PGSI_SMALL_MAX")) h->small_max = atoll(getenv("PGSI_SMALL_MAX"));
     if (cudaDeviceGetAttribute(&h->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device) != cudaSuccess)
         h->smem_optin = 48 * 1024;
+    G.inc_e_in_v2 = getenv("PGSI_INC_E_V2") ? atoi(getenv("PGSI_INC_E_V2")) : 1;
     G.inc_fuse_e = getenv("PGSI_INC_FUSE_E") ? atoi(getenv("PGSI_INC_FUSE_E")) : 0;   // measured slower
     G.inc_skip_v1 = getenv("PGSI_INC_SKIP_V1") ? atoi(getenv("PGSI_INC_SKIP_V1")) : 1;
     G.inc_blk_frontier = getenv("PGSI_INC_BLK") ? atoi(getenv("PGSI_INC_BLK")) : 256;

@@ -142,6 +142,7 @@ struct DevGame {
     int64_t inc_s_div;      // incremental step only while |S| * inc_s_div <= n'
     int32_t inc_s_odd;      // the switch list S of the first incremental step came from All_Odd
     int32_t inc_fuse_e;     // build E inside the dirty-closure scan (else a separate pass)
+    int32_t inc_e_in_v2;    // build E in the V2-on-D pass (else a separate pass)
     int32_t inc_skip_v1;    // after All_Odd steps replace V1 on D by the V2 walk depth
     int32_t inc_blk_frontier; // closure levels with at most this many frontier vertices run in block 0
 };

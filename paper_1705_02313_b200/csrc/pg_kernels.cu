@@ -1360,54 +1360,62 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
 #pragma unroll
     for (int k = 0; k < 32; k++) hb[k] = 0;
     unsigned long long wsteps = 0;
-    for (int64_t b0 = wbase; b0 < nd; b0 += stride) {   // warp-uniform (warp_append)
+    // E (step 4) is built in the same pass over D when inc_e_in_v2: each D vertex's
+    // reverse range is scanned right after its walk, saving a grid barrier and a
+    // second pass over the D list
+    const bool e_in_v2 = g.inc_e_in_v2 && !g.inc_fuse_e;
+    for (int64_t b0 = wbase; b0 < nd; b0 += stride) {   // warp-uniform (warp_append, expand_rev)
         const int64_t i = b0 + lane;
         const int32_t v = i < nd ? __ldcg(g.Dl + i) : -1;
+        uint2 rr = make_uint2(0u, 0u);
+        if (e_in_v2 && v >= 0) rr = __ldcg(g.Dr + i);
         if (odd_s) {
             const bool addc = v >= 0 && __ldcg(g.cmark + v) != g.cepoch;
             if (addc) g.cmark[v] = g.cepoch;
             warp_append(addc, v, g.Cl, &ctl->nC);
         }
-        if (v < 0) continue;
-        bool fin = true;
-        if (!odd_s) {
-            const unsigned long long e = __ldcg(jl + v);
-            fin = (uint32_t)e == SINK;
-        }
-        g.top[v] = fin ? 0 : 1;
-        if (!fin) {
-            put_cpx(g, v, make_uint4(1u, 0, 0, 0), make_uint4(0, 0, 0, 0));
-            continue;
-        }
-        uint32_t mask = 0, steps = 0;
-        int32_t x = v;
-        while (x != (int32_t)N && __ldcg(g.dmark + x) == ep) {
-            const uint32_t p = __ldg(g.pidx + x);
-            x = __ldg(g.succ + x);
-            if (++hb[p] == 255) { atomicOr(&ctl->inc_overflow, 1ull); break; }
-            mask |= 1u << p;
-            steps++;
-        }
-        wsteps += steps;
-        if (odd_s) {   // depth(v) = steps + depth(x); x is clean (final jl) or the sink
-            uint32_t dx = 0;
-            if (x != (int32_t)N) {
-                const unsigned long long ex = __ldcg(jl + x);
-                if ((uint32_t)ex != SINK) atomicOr(&ctl->inc_overflow, 1ull);   // clean ⊤ exit: redo in full
-                dx = (uint32_t)(ex >> 32);
+        if (v >= 0) {
+            bool fin = true;
+            if (!odd_s) {
+                const unsigned long long e = __ldcg(jl + v);
+                fin = (uint32_t)e == SINK;
             }
-            uint32_t dv = steps + dx;
-            if (dv > 0x7fffffffu) dv = 0x7fffffffu;
-            jl[v] = pack_jl(SINK, dv);
+            g.top[v] = fin ? 0 : 1;
+            if (!fin) {
+                put_cpx(g, v, make_uint4(1u, 0, 0, 0), make_uint4(0, 0, 0, 0));
+            } else {
+                uint32_t mask = 0, steps = 0;
+                int32_t x = v;
+                while (x != (int32_t)N && __ldcg(g.dmark + x) == ep) {
+                    const uint32_t p = __ldg(g.pidx + x);
+                    x = __ldg(g.succ + x);
+                    if (++hb[p] == 255) { atomicOr(&ctl->inc_overflow, 1ull); break; }
+                    mask |= 1u << p;
+                    steps++;
+                }
+                wsteps += steps;
+                if (odd_s) {   // depth(v) = steps + depth(x); x is clean (final jl) or the sink
+                    uint32_t dx = 0;
+                    if (x != (int32_t)N) {
+                        const unsigned long long ex = __ldcg(jl + x);
+                        if ((uint32_t)ex != SINK) atomicOr(&ctl->inc_overflow, 1ull);   // clean ⊤ exit: redo in full
+                        dx = (uint32_t)(ex >> 32);
+                    }
+                    uint32_t dv = steps + dx;
+                    if (dv > 0x7fffffffu) dv = 0x7fffffffu;
+                    jl[v] = pack_jl(SINK, dv);
+                }
+                cpx_merge_store(g, v, hb, mask, x, ow);
+            }
         }
-        cpx_merge_store(g, v, hb, mask, x, ow);
+        if (e_in_v2) expand_rev<1>(g, -1, rr.x, rr.y, g.emark, ep, g.El, &ctl->nE);
     }
     gbar(ctl);
 
     // ---- 4. E = Odd vertices with a candidate in D: built by the closure scan
     // (inc_fuse_e) or by a pass over D's reverse edges
     trace_ts(g, 4);
-    if (!g.inc_fuse_e) {
+    if (!g.inc_fuse_e && !e_in_v2) {
         for (int64_t b0 = wbase; b0 < nd; b0 += stride) {
             const int64_t i = b0 + lane;
             uint32_t rb = 0, re = 0;
