@@ -98,5 +98,12 @@ if bench_line:
     import bench  # noqa: E402
     line = json.loads(open(bench_line).read().strip().splitlines()[-1])
     line["hbm_actual"] = bench.ncu_dram_summary(line["roofline"]["peak"])
+    kname = {"k_inc_iter (incremental valuation + All_Odd over E)": "k_inc_iter", "k_v1 (full V1)": "k_v1",
+             "k_spl_* + k_v2_cpx (full V2)": "k_v2_cpx"}.get(line["roofline"]["kernel"])
+    if kname:
+        line["roofline"]["traffic"], line["roofline"]["traffic_source"] = bench.ncu_traffic(kname)
+    bf = (line.get("arms") or {}).get("bf", {}).get("roofline")
+    if bf:
+        bf["traffic"], bf["traffic_source"] = bench.ncu_traffic("k_bf_round")
     open(os.path.join(dst, "bench_cfg3.json"), "w").write(json.dumps(line) + "\n")
 print("ok:", dst)
