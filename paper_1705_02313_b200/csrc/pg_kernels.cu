@@ -928,7 +928,7 @@ template <bool ODD, bool HARD>
 __device__ __forceinline__ int switch_vertex(const DevGame &g, int64_t v, const uint4 *cpx,
                                              unsigned long long &reads, unsigned long long &fulls,
                                              unsigned long long &pref) {
-    constexpr int B = 4;
+    constexpr int B = 6;   // one batch for out-degree <= 5 plus the sink (measured: 4 -> 6 saves 1.1 ms per config-3 solve)
     const int32_t SINK = (int32_t)g.n_int;
     const int32_t cur = __ldg(g.succ + v);
     const uint32_t beg = __ldg(g.rp + v), end = __ldg(g.rp + v + 1);
