@@ -64,6 +64,9 @@ def _load():
         L.oracle_solve_mode.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_int64, P, P, P, P, P, P,
                                         P, P, P, C.c_int64, P, C.c_int64]
         L.oracle_solve_mode.restype = C.c_int
+        L.oracle_solve_traced.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_int64, P, P, P, P, P, P,
+                                          P, P, P, C.c_int64, P]
+        L.oracle_solve_traced.restype = C.c_int
         L.oracle_best_response_bf.argtypes = [C.c_void_p, P, P, P, P, P]
         L.oracle_best_response_bf.restype = C.c_int
         L.oracle_switch_step.argtypes = [C.c_void_p, P, C.c_int, P, P]
@@ -89,6 +92,7 @@ class SolveResult:
     outer_passes: int
     odd_trace: np.ndarray
     even_trace: np.ndarray
+    trace: np.ndarray | None = None   # per-iteration parity trace, uint64 [records, 5]
 
 
 class Oracle:
@@ -191,6 +195,28 @@ class Oracle:
         inner, outer = int(stats[0]), int(stats[1])
         return SolveResult(winner, sigma, tau, val, succ_int, val_int, top_int, inner, outer,
                            ot[:min(inner, trace_cap)].copy(), et[:min(outer, trace_cap)].copy())
+
+    def solve_traced(self, max_inner: int = 0, max_outer: int = 0, mode: str = "si",
+                     cap: int = 1 << 16) -> SolveResult:
+        """solve() plus the per-iteration parity trace: one record
+        (0, h_succ, h_val, n_top, odd switches) per valuation and (1, 0, 0, 0, even
+        switches) per All_Even step, as uint64 [records, 5]."""
+        n, N, d = self.n, self.n_internal, self.d
+        winner = np.zeros(n, np.uint8)
+        sigma = np.zeros(n, np.int32)
+        tau = np.zeros(n, np.int32)
+        val = np.zeros((n, d), np.int32)
+        succ_int = np.zeros(N, np.int32)
+        top_int = np.zeros(N, np.uint8)
+        stats = np.zeros(8, np.int64)
+        tr = np.zeros((cap, 5), np.uint64)
+        tl = np.zeros(1, np.int64)
+        self._check(_load().oracle_solve_traced(self._h, self.MODES[mode], max_inner, max_outer, _p(winner),
+                                                _p(sigma), _p(tau), _p(val), _p(succ_int), None,
+                                                _p(top_int), _p(stats), _p(tr), cap, _p(tl)))
+        inner, outer = int(stats[0]), int(stats[1])
+        return SolveResult(winner, sigma, tau, val, succ_int, None, top_int, inner, outer,
+                           np.zeros(0, np.int64), np.zeros(0, np.int64), tr[:min(int(tl[0]), cap)].copy())
 
     def switch_step(self, succ, side: int):
         out = np.zeros(self.n_internal, np.int32)

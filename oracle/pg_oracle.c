@@ -400,15 +400,68 @@ int oracle_valuate(const og_game *g, const int32_t *strategy, int32_t *val, uint
     return OR_OK;
 }
 
+/* ------------------------------------------------------------------------ */
+/* Per-iteration parity trace (SURVEY.md §8(c) "Per-iteration parity trace"):  */
+/* a CHECKER, not part of the method. After every valuation of Algorithm 1's  */
+/* inner loop one record {0, h_succ, h_val, n_top, odd switches}; after every */
+/* All_Even step one record {1, 0, 0, 0, even switches}. Over ABI-order       */
+/* vertices v (sink successor = 2^32-1), with mix64 the splitmix64 finalizer: */
+/*   h_succ = Σ_v mix64(v·2^32 + succ(v))                     (mod 2^64)      */
+/*   h_val  = Σ_{v finite} mix64(v·2^32 + Σ_i (i+1)·val(v)[i]·K_i)            */
+/*   K_i    = mix64(0x9E3779B97F4A7C15 · (i+1))                               */
+/* The CUDA path computes the same records independently (pg_get_trace).      */
+/* ------------------------------------------------------------------------ */
+#define OR_TRACE_WORDS 5
+typedef struct {
+    uint64_t *rec;      /* cap records of OR_TRACE_WORDS words */
+    int64_t cap, len;
+} og_trace;
+
+static uint64_t og_mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+static void og_trace_put(og_trace *t, uint64_t kind, uint64_t hs, uint64_t hv, uint64_t ntop, uint64_t sw) {
+    if (!t) return;
+    if (t->len < t->cap) {
+        uint64_t *r = t->rec + t->len * OR_TRACE_WORDS;
+        r[0] = kind; r[1] = hs; r[2] = hv; r[3] = ntop; r[4] = sw;
+    }
+    t->len++;
+}
+
+/* hashes of the valuated profile succ and its valuation V (plain loops) */
+static void og_trace_hash(const og_game *g, const int32_t *succ, const og_vals *V,
+                          uint64_t *hs, uint64_t *hv, uint64_t *ntop) {
+    uint64_t a = 0, b = 0, c = 0;
+    for (int64_t v = 0; v < g->n_int; v++) {
+        uint64_t s = succ[v] == SINK ? 0xFFFFFFFFull : (uint64_t)(uint32_t)succ[v];
+        a += og_mix64(((uint64_t)v << 32) + s);
+        if (V->top[v]) { c++; continue; }
+        uint64_t lin = 0;
+        for (int32_t i = 0; i < g->d; i++)
+            lin += (uint64_t)(i + 1) * (uint64_t)(uint32_t)V->val[v * g->d + i] *
+                   og_mix64(0x9E3779B97F4A7C15ull * (uint64_t)(i + 1));
+        b += og_mix64(((uint64_t)v << 32) + lin);
+    }
+    *hs = a; *hv = b; *ntop = c;
+}
+
 /* inner loop of Algorithm 1: one-player SI for Odd.
  * odd_trace (optional, cap entries): number of Odd switches per valuation. */
 static int og_inner(const og_game *g, int32_t *succ, og_vals *V, int64_t *inner,
-                    int64_t max_inner, int64_t *odd_trace, int64_t trace_cap, int64_t *trace_len) {
+                    int64_t max_inner, int64_t *odd_trace, int64_t trace_cap, int64_t *trace_len,
+                    og_trace *tr) {
     for (;;) {
         if (max_inner > 0 && *inner >= max_inner) { set_err("inner iteration cap"); return OR_EITERCAP; }
         if (og_valuate(g, succ, V)) { set_err("odd cycle: strategy not admissible"); return OR_EINADMISSIBLE; }
         (*inner)++;
+        uint64_t hs = 0, hv = 0, nt = 0;
+        if (tr) og_trace_hash(g, succ, V, &hs, &hv, &nt);
         int64_t c = og_odd_switch(g, V, succ);
+        og_trace_put(tr, 0, hs, hv, nt, (uint64_t)c);
         if (odd_trace && *trace_len < trace_cap) odd_trace[*trace_len] = c;
         (*trace_len)++;
         if (c == 0) return OR_OK;
@@ -527,7 +580,7 @@ int oracle_best_response(const og_game *g, const int32_t *sigma, const int32_t *
     og_vals V;
     og_alloc_vals(g, &V);
     int64_t inner = 0, tl = 0;
-    rc = og_inner(g, succ, &V, &inner, 0, NULL, 0, &tl);
+    rc = og_inner(g, succ, &V, &inner, 0, NULL, 0, &tl, NULL);
     if (tau_out) for (int64_t v = 0; v < g->n_int; v++) tau_out[v] = g->owner[v] == 1 ? succ[v] : -2;
     og_copy_out(g, &V, val, top, NULL, g->n_int);
     if (inner_iters) *inner_iters = inner;
@@ -552,10 +605,11 @@ int oracle_best_response(const og_game *g, const int32_t *sigma, const int32_t *
 #define OR_MODE_SI 0        /* Algorithm 1: τ warm-started from the previous best response */
 #define OR_MODE_SI_RESET 1  /* SI-Reset: τ := τ_init before every best response */
 #define OR_MODE_BF 2        /* best responses by Bellman-Ford; inner = rounds */
-int oracle_solve_mode(const og_game *g, int mode, int64_t max_inner, int64_t max_outer,
-                      uint8_t *winner, int32_t *sigma, int32_t *tau, int32_t *val,
-                      int32_t *succ_int, int32_t *val_int, uint8_t *top_int, int64_t *stats,
-                      int64_t *odd_trace, int64_t odd_cap, int64_t *even_trace, int64_t even_cap) {
+static int og_solve(const og_game *g, int mode, int64_t max_inner, int64_t max_outer,
+                    uint8_t *winner, int32_t *sigma, int32_t *tau, int32_t *val,
+                    int32_t *succ_int, int32_t *val_int, uint8_t *top_int, int64_t *stats,
+                    int64_t *odd_trace, int64_t odd_cap, int64_t *even_trace, int64_t even_cap,
+                    og_trace *tr) {
     int64_t N = g->n_int;
     int32_t *succ = malloc(sizeof(int32_t) * ((size_t)N + 1));
     /* σ_init(v) = s for Even; τ arbitrary = first successor (reading 4) */
@@ -569,11 +623,12 @@ int oracle_solve_mode(const og_game *g, int mode, int64_t max_inner, int64_t max
         if (mode == OR_MODE_SI_RESET && outer > 0)       /* SI-Reset: τ := τ_init */
             for (int64_t v = 0; v < N; v++) if (g->owner[v] == 1) succ[v] = g->adj[g->adj_ptr[v]];
         if (mode == OR_MODE_BF) rc = og_bellman_ford(g, succ, &V, &inner, max_inner);
-        else rc = og_inner(g, succ, &V, &inner, max_inner, odd_trace, odd_cap, &otl);
+        else rc = og_inner(g, succ, &V, &inner, max_inner, odd_trace, odd_cap, &otl, tr);
         if (rc) break;
         outer++;
         int64_t c = og_even_switch(g, &V, succ);          /* σ := σ[All_Even(σ)] */
         if (even_trace && etl < even_cap) even_trace[etl] = c;
+        og_trace_put(tr, 1, 0, 0, 0, (uint64_t)c);
         etl++;
         if (c == 0) break;                                /* until S_Even = ∅ */
     }
@@ -598,6 +653,28 @@ int oracle_solve_mode(const og_game *g, int mode, int64_t max_inner, int64_t max
     }
     og_free_vals(&V);
     free(succ);
+    return rc;
+}
+
+int oracle_solve_mode(const og_game *g, int mode, int64_t max_inner, int64_t max_outer,
+                      uint8_t *winner, int32_t *sigma, int32_t *tau, int32_t *val,
+                      int32_t *succ_int, int32_t *val_int, uint8_t *top_int, int64_t *stats,
+                      int64_t *odd_trace, int64_t odd_cap, int64_t *even_trace, int64_t even_cap) {
+    return og_solve(g, mode, max_inner, max_outer, winner, sigma, tau, val, succ_int, val_int, top_int,
+                    stats, odd_trace, odd_cap, even_trace, even_cap, NULL);
+}
+
+/* oracle_solve_mode plus the per-iteration parity trace (og_trace above):
+ * trace = cap records of 5 uint64 words; *trace_len = records produced (may
+ * exceed cap; only the first cap are stored). */
+int oracle_solve_traced(const og_game *g, int mode, int64_t max_inner, int64_t max_outer,
+                        uint8_t *winner, int32_t *sigma, int32_t *tau, int32_t *val, int32_t *succ_int,
+                        int32_t *val_int, uint8_t *top_int, int64_t *stats, uint64_t *trace, int64_t cap,
+                        int64_t *trace_len) {
+    og_trace t = {trace, cap, 0};
+    int rc = og_solve(g, mode, max_inner, max_outer, winner, sigma, tau, val, succ_int, val_int, top_int,
+                      stats, NULL, 0, NULL, 0, &t);
+    if (trace_len) *trace_len = t.len;
     return rc;
 }
 

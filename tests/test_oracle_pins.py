@@ -345,6 +345,32 @@ def test_ties_never_switch():
     assert tau[0] == 2 and inner == 1
 
 
+def test_odd_switch_takes_first_of_tied_minima():
+    """Reading 3 for All_Odd ("arbitrarily", 542-546 ⊑-minimal
+    target): among tied ⊑-minimal successors Odd takes the FIRST in canonical
+    adjacency order. Hand trace: Odd v (pri 0) with adj [c, a, b] in id order, where
+    a, b are Even pri 2 on the sink (val {2:1} each) and c is Even pri 4 on the sink
+    (val {4:1}). val(a) = val(b) ⊏ val(c) (maxdiff 4 is even and c counts more), so
+    from τ(v) = c the switch goes to a, never to b."""
+    # ids: v = 0 (Odd, pri 0), c = 1 (Even, pri 4), a = 2 and b = 3 (Even, pri 2)
+    g = gi.from_adjacency([1, 0, 0, 0], [0, 4, 2, 2], [[1, 2, 3], [0], [0], [0]])
+    o = Oracle(g, preprocess=False)
+    out, c = o.switch_step(np.array([1, -1, -1, -1], np.int32), 1)
+    assert out[0] == 2 and c == 1
+    # with the tied pair first: adj [a, b, c] -> a
+    g = gi.from_adjacency([1, 0, 0, 0], [0, 2, 2, 4], [[1, 2, 3], [0], [0], [0]])
+    o = Oracle(g, preprocess=False)
+    out, c = o.switch_step(np.array([3, -1, -1, -1], np.int32), 1)
+    assert out[0] == 1 and c == 1
+    # through the inner loop (σ = sink everywhere): τ0 = c -> a after one switch;
+    # the second valuation finds no Odd-switchable edge: 2 valuations
+    g = gi.from_adjacency([1, 0, 0, 0], [0, 4, 2, 2], [[1, 2, 3], [0], [0], [0]])
+    tau, val, top, inner = Oracle(g).best_response(np.array([0, -1, -1, -1], np.int32),
+                                                   np.array([1, 0, 0, 0], np.int32))
+    assert tau[0] == 2 and inner == 2
+    assert top[0] == 0 and list(val[0]) == [1, 1, 0]   # D = {0, 2, 4}: {0:1, 2:1}
+
+
 # ------------------------------- SI-Reset and Bellman-Ford arms (§8(f) F2)
 @pytest.mark.parametrize("seed", range(40))
 def test_bf_best_response_matches_reference_bf(seed):
@@ -434,3 +460,47 @@ def test_bf_no_preprocess_inadmissible():
     with pytest.raises(OracleError) as e:
         o.solve(mode="bf")
     assert e.value.name == "EINADMISSIBLE"
+
+
+# ---------------------------- per-iteration parity trace
+def _trace_hash(succ, val, top):
+    """h_succ, h_val, n_top of SURVEY.md §8(c), written out with numpy (the checker's
+    definition; the oracle's C loops compute it independently)."""
+    N, d = val.shape
+    v = np.arange(N, dtype=np.uint64)
+    s = np.where(succ < 0, np.uint64(0xFFFFFFFF), succ.astype(np.int64).astype(np.uint64))
+    with np.errstate(over="ignore"):
+        hs = int(gi.mix64((v << np.uint64(32)) + s).sum(dtype=np.uint64))
+        i1 = np.arange(1, d + 1, dtype=np.uint64)
+        K = gi.mix64(np.uint64(0x9E3779B97F4A7C15) * i1)
+        lin = (val.astype(np.uint64) * (i1 * K)[None, :]).sum(axis=1, dtype=np.uint64)
+        fin = top == 0
+        hv = int(gi.mix64((v[fin] << np.uint64(32)) + lin[fin]).sum(dtype=np.uint64))
+    return hs, hv, int((top != 0).sum())
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_trace_consistent_with_solve(seed):
+    """The trace has one record per valuation (inner) and per All_Even step (outer),
+    in Algorithm 1's order; its switch counts are the solve's
+    per-iteration counts; its last valuation record hashes the final profile and
+    val^{σ*} as exported by the solve."""
+    rng = np.random.default_rng(900 + seed)
+    n = int(rng.integers(1, 400))
+    g = gi.random_game(n, int(rng.integers(1, 9)), 1, min(4, n), seed)
+    o = Oracle(g)
+    r = o.solve()
+    t = o.solve_traced()
+    assert len(t.trace) == r.inner_iters + r.outer_passes
+    kinds = t.trace[:, 0]
+    assert int((kinds == 0).sum()) == r.inner_iters and int((kinds == 1).sum()) == r.outer_passes
+    assert kinds[-1] == 1
+    np.testing.assert_array_equal(t.trace[kinds == 0, 4].astype(np.int64), r.odd_trace)
+    np.testing.assert_array_equal(t.trace[kinds == 1, 4].astype(np.int64), r.even_trace)
+    # the record before the final All_Even step valuates the final profile
+    last = t.trace[-2]
+    assert last[0] == 0 and last[4] == 0
+    assert tuple(int(x) for x in last[1:4]) == _trace_hash(r.succ_int, r.val_int, r.top_int)
+    # identical solve outputs with and without the trace
+    np.testing.assert_array_equal(t.tau, r.tau)
+    np.testing.assert_array_equal(t.val, r.val)
