@@ -96,11 +96,16 @@ enum {
     PG_SI_RESET = 128,        /* SI-Reset: τ := τ_init (first successor) before every best
                                  response instead of warm-starting from the previous one
                                                                        */
-    PG_BELLMAN_FORD = 256     /* best responses by Bellman-Ford:
+    PG_BELLMAN_FORD = 256,    /* best responses by Bellman-Ford:
                                  synchronous relaxation rounds from ⊤ until a round changes
                                  nothing; inner_iters counts rounds; τ = first ⊑-minimal
                                  successor at the fixpoint (reading 19). Takes
                                  precedence over PG_SI_RESET                              */
+    PG_TRACE = 512            /* record the per-iteration parity trace of pg_solve /
+                                 pg_best_response; read it with
+                                 pg_get_trace. A checker: one valuation per launch, no
+                                 whole-solve kernel, plus O(n' log n') hash work per
+                                 valuation. Results are unchanged                         */
 };
 
 typedef struct {
@@ -329,6 +334,26 @@ pg_status pg_verify_solution_device(int64_t n, const int64_t *row_ptr, const int
                                     const uint8_t *owner, const int32_t *priority, const uint8_t *winner,
                                     const int32_t *sigma, const int32_t *tau, int32_t device,
                                     int64_t *witness, int64_t *rounds);
+
+/* pg_get_trace: the per-iteration parity trace of the last pg_solve /
+ * pg_best_response call on a handle loaded with PG_TRACE (a checker
+ * for localising a divergence from the oracle, which computes the same records).
+ * Records of 5 uint64 words, in call order:
+ *   after every valuation of the inner loop:
+ *     {0, h_succ, h_val, n_top, Odd switches of the All_Odd step that follows}
+ *   after every All_Even step:  {1, 0, 0, 0, Even switches}
+ * with, over ABI-order vertices v (a successor in ABI order, the sink = 2^32-1),
+ * mix64 = the splitmix64 finalizer and arithmetic mod 2^64:
+ *   h_succ = Σ_v mix64(v·2^32 + succ(v))          over the valuated profile σ ∪ τ
+ *   h_val  = Σ_{v finite} mix64(v·2^32 + Σ_i (i+1)·val(v)[i]·K_i),
+ *   K_i    = mix64(0x9E3779B97F4A7C15·(i+1)),     val(v)[i] = count of D[i]
+ *   n_top  = #{v : val(v) = ⊤}
+ * Bellman-Ford best responses (PG_BELLMAN_FORD) record no valuation entries.
+ *   records      uint64[cap*5] or NULL (host pointer)
+ *   len          receives the number of records of the last call (may exceed cap;
+ *                only min(len, cap) are written)
+ * Errors: PG_EINVAL (NULL handle or len), PG_ESTATE if the handle has no trace. */
+pg_status pg_get_trace(pg_game g, uint64_t *records, int64_t cap, int64_t *len);
 
 /* pg_get_stats: statistics of the last call on the handle (host pointer). */
 pg_status pg_get_stats(pg_game g, pg_stats *stats);

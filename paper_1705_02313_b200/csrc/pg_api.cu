@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "pg_internal.cuh"
+#include "pg_guard.h"
 
 using namespace pgsi;
 
@@ -74,6 +75,12 @@ struct pg_game_s {
     int smem_optin = 0;               // max dynamic shared memory per block (bytes)
     // Bellman-Ford arm (PG_BELLMAN_FORD): double-buffered key rows (⊤ = all INT_MAX)
     int32_t *bf_row[2] = {nullptr, nullptr};
+    // per-iteration parity trace (PG_TRACE; pg_trace.cu): records of 5 words
+    std::vector<uint64_t> ptrace;
+    int32_t *tsucc = nullptr;                 // the profile a traced step valuates
+    unsigned long long *tL[2] = {nullptr, nullptr};
+    int32_t *tJ[2] = {nullptr, nullptr};
+    unsigned long long *tout = nullptr;       // device h_succ, h_val, n_top
 };
 
 #define CK(h, x)                                                                         \
@@ -183,6 +190,7 @@ void reset_call_stats(pg_game h) {
     h->st.d = keep.d;
     h->st.dummies = keep.dummies;
     h->st.ms_load = keep.ms_load;
+    h->ptrace.clear();
     h->recs.clear();
     h->ev_used = 0;
 }
@@ -275,6 +283,33 @@ pg_status valuate_dev(pg_game h, bool want_cdom, bool full_rows, bool inc = fals
 pg_status readback(pg_game h) {
     CK(h, cudaMemcpyAsync(h->h_ctl, h->G.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, h->stream));
     CK(h, cudaStreamSynchronize(h->stream));
+    return PG_OK;
+}
+
+// PG_TRACE: keep the profile a step valuates (the step applies its switches).
+pg_status trace_begin(pg_game h) {
+    const size_t N1 = (size_t)h->G.n_int + 1;
+    if (!h->tsucc) {
+        CK(h, dalloc(h, &h->tsucc, N1));
+        for (int b = 0; b < 2; b++) {
+            CK(h, dalloc(h, &h->tL[b], N1));
+            CK(h, dalloc(h, &h->tJ[b], N1));
+        }
+        CK(h, dalloc(h, &h->tout, 4));
+    }
+    CK(h, cudaMemcpyAsync(h->tsucc, h->G.succ, sizeof(int32_t) * N1, cudaMemcpyDeviceToDevice, h->stream));
+    return PG_OK;
+}
+
+// PG_TRACE: hash the step's profile and its valuation (top / values are final for
+// the pre-step profile after any step) and append {0, h_succ, h_val, n_top, switches}.
+pg_status trace_end(pg_game h, uint64_t switches) {
+    CK(h, launch_trace_hash(h->G, h->lc.sms, h->tsucc, h->tL[0], h->tL[1], h->tJ[0], h->tJ[1], h->tout,
+                            h->stream));
+    unsigned long long r[3];
+    CK(h, cudaMemcpyAsync(r, h->tout, sizeof(r), cudaMemcpyDeviceToHost, h->stream));
+    CK(h, cudaStreamSynchronize(h->stream));
+    for (uint64_t w : {(uint64_t)0, (uint64_t)r[0], (uint64_t)r[1], (uint64_t)r[2], switches}) h->ptrace.push_back(w);
     return PG_OK;
 }
 
@@ -394,8 +429,14 @@ pg_status valuate_and_switch(pg_game h, bool odd, bool want_cdom, bool do_switch
     const bool bfs_ok = do_switch && h->G.dp <= 32 && (h->flags & PG_BFS) &&
                         h->last_maxdepth * 4 < (int64_t)h->G.bfs_max_levels * 3;
     bool bfs = !inc && bfs_ok;
-    if (h->dist_fn || h->G.trace_ts) max_steps = 1;   // sharded: the host exchanges S every step
+    const bool traced = do_switch && (h->flags & PG_TRACE);
+    // sharded: the host exchanges S every step; traced: every valuation is hashed
+    if (h->dist_fn || h->G.trace_ts || traced) max_steps = 1;
     max_steps = std::min<int64_t>(max_steps, h->inc_max_steps);
+    if (traced) {
+        pg_status rc = trace_begin(h);
+        if (rc) return rc;
+    }
     const double t_start = h->trace ? now_ms() : 0.0;
     int64_t done_inc = 0;      // inner iterations completed by an incremental launch that then aborted
     for (;;) {
@@ -431,6 +472,10 @@ pg_status valuate_and_switch(pg_game h, bool odd, bool want_cdom, bool do_switch
     }
     if (do_switch) {
         pg_status rc = dist_exchange(h, odd);
+        if (rc) return rc;
+    }
+    if (traced) {
+        pg_status rc = trace_end(h, inc ? h->h_ctl->last_sw : h->h_ctl->odd_switches);
         if (rc) return rc;
     }
     h->have_state = true;
@@ -590,6 +635,8 @@ pg_status even_switch(pg_game h, int64_t *count) {
     if (rc) return rc;
     if ((rc = dist_exchange(h, false))) return rc;
     *count = (int64_t)h->h_ctl->even_switches;
+    if (h->flags & PG_TRACE)
+        for (uint64_t w : {(uint64_t)1, (uint64_t)0, (uint64_t)0, (uint64_t)0, (uint64_t)*count}) h->ptrace.push_back(w);
     h->last_nsw = (int64_t)h->h_ctl->nswl;
     h->last_sw_odd = false;
     if (h->trace) fprintf(stderr, "[pgsi] even switch: inc=%d |C|=%llu |E|=%llu %lld switches\n", (int)inc,
@@ -697,7 +744,7 @@ const char *pg_last_error(void) { return t_err.c_str(); }
 
 const char *pg_version(void) { return "pgsi-b200 0.1 (sm_100a)"; }
 
-void pg_free(pg_game h) {
+void pg_free(pg_game h) try {
     if (!h) return;
     DeviceGuard dg(h->device);
     for (void *p : h->allocs) {
@@ -710,10 +757,11 @@ void pg_free(pg_game h) {
     for (auto e : h->ev_pool) cudaEventDestroy(e);
     if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
     delete h;
+} catch (...) {
 }
 
 pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const uint8_t *owner,
-                  const int32_t *priority, const pg_options *opt, pg_game *out) {
+                  const int32_t *priority, const pg_options *opt, pg_game *out) try {
     if (!out) { set_err("NULL out"); return PG_EINVAL; }
     *out = nullptr;
     double t0 = now_ms();
@@ -758,7 +806,32 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     int64_t host_max = 32768;
     if (getenv("PGSI_HOST_LOAD_MAX")) host_max = atoll(getenv("PGSI_HOST_LOAD_MAX"));
     const int64_t m_in = (n > 0 && row_ptr) ? row_ptr[n] : 0;
-    if ((o.flags & PG_HOST_LOAD) || n + m_in <= host_max) {
+    bool host_load = (o.flags & PG_HOST_LOAD) || n + m_in <= host_max;
+    if (!host_load) {
+        auto persist = [h](size_t bytes) -> void * {
+            void *p = nullptr;
+            if (cudaMallocAsync(&p, std::max<size_t>(bytes, 16), h->stream) != cudaSuccess) return nullptr;
+            h->allocs.push_back(p);
+            return p;
+        };
+        pg_status rc = build_device_game(n, row_ptr, col, owner, priority, preprocess, s, persist, L, err);
+        if (rc == PG_ENOTSUP && L.n_int == 0) {
+            // a limit of the device transform only (e.g. priority values >= 2^26, which
+            // its radix keys cannot hold): the host transform accepts the game
+            for (void *p : h->allocs) cudaFreeAsync(p, s);
+            h->allocs.clear();
+            host_load = true;
+            err.clear();
+        } else if (rc) {
+            set_err(err);
+            return fail(rc);
+        } else {
+            uint32_t rpe = 0;
+            CKL(cudaMemcpy(&rpe, L.rp + L.n_even, 4, cudaMemcpyDeviceToHost));
+            L.m_odd = (int64_t)L.m_int - (int64_t)rpe;
+        }
+    }
+    if (host_load) {
         HostGame H;
         pg_status rc = build_host_game(n, row_ptr, col, owner, priority, preprocess, H, err);
         if (rc) { set_err(err); return fail(rc); }
@@ -787,18 +860,6 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
         L.d = H.d; L.D = H.D; L.rp = rp; L.col = colp; L.pidx = pidx; L.perm = perm; L.iperm = iperm;
         L.proj = proj; L.rrp = rrp; L.rcol = rcol;
         L.m_odd = (int64_t)H.m_int - (int64_t)H.rp[H.n_even];
-    } else {
-        auto persist = [h](size_t bytes) -> void * {
-            void *p = nullptr;
-            if (cudaMallocAsync(&p, std::max<size_t>(bytes, 16), h->stream) != cudaSuccess) return nullptr;
-            h->allocs.push_back(p);
-            return p;
-        };
-        pg_status rc = build_device_game(n, row_ptr, col, owner, priority, preprocess, s, persist, L, err);
-        if (rc) { set_err(err); return fail(rc); }
-        uint32_t rpe = 0;
-        CKL(cudaMemcpy(&rpe, L.rp + L.n_even, 4, cudaMemcpyDeviceToHost));
-        L.m_odd = (int64_t)L.m_int - (int64_t)rpe;
     }
     h->n = n;
     h->m = L.m;
@@ -909,21 +970,21 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     h->st.ms_load = now_ms() - t0;
     *out = h;
     return PG_OK;
-}
+} PGSI_ABI_CATCH
 
-pg_status pg_info(pg_game h, int64_t *n_internal, int32_t *d, int32_t *priorities, int64_t *dummies) {
+pg_status pg_info(pg_game h, int64_t *n_internal, int32_t *d, int32_t *priorities, int64_t *dummies) try {
     if (!h) { set_err("NULL handle"); return PG_EINVAL; }
     if (n_internal) *n_internal = h->G.n_int;
     if (d) *d = (int32_t)h->D.size();
     if (priorities) std::memcpy(priorities, h->D.data(), sizeof(int32_t) * h->D.size());
     if (dummies) *dummies = h->dummies;
     return PG_OK;
-}
+} PGSI_ABI_CATCH
 
 pg_status pg_inspect(int64_t n, const int64_t *row_ptr, const int32_t *col, const uint8_t *owner,
                      const int32_t *priority, uint32_t flags, int64_t *n_internal, int32_t *d,
                      int64_t *dummies, int64_t *m_internal, uint8_t *owner_int, int32_t *pidx_int,
-                     int64_t *adj_ptr, int32_t *adj, int32_t *priorities) {
+                     int64_t *adj_ptr, int32_t *adj, int32_t *priorities) try {
     HostGame H;
     std::string err;
     pg_status rc = build_host_game(n, row_ptr, col, owner, priority, !(flags & PG_NO_PREPROCESS), H, err);
@@ -946,9 +1007,9 @@ pg_status pg_inspect(int64_t n, const int64_t *row_ptr, const int32_t *col, cons
     }
     if (adj_ptr) adj_ptr[H.n_int] = o;
     return PG_OK;
-}
+} PGSI_ABI_CATCH
 
-pg_status pg_dist_attach(pg_game h, int32_t rank, int32_t world, pg_allgather_fn fn, void *ctx) {
+pg_status pg_dist_attach(pg_game h, int32_t rank, int32_t world, pg_allgather_fn fn, void *ctx) try {
     pg_status rc = check_handle(h);
     if (rc) return rc;
     if (world < 1 || rank < 0 || rank >= world) { set_err("pg_dist_attach: need 0 <= rank < world"); return PG_EINVAL; }
@@ -980,15 +1041,25 @@ pg_status pg_dist_attach(pg_game h, int32_t rank, int32_t world, pg_allgather_fn
     span(G.n_even, G.n_int - G.n_even, G.sh_odd_lo, G.sh_odd_hi);
     G.sharded = 1;
     return PG_OK;
-}
+} PGSI_ABI_CATCH
 
-pg_status pg_get_stats(pg_game h, pg_stats *stats) {
+pg_status pg_get_trace(pg_game h, uint64_t *records, int64_t cap, int64_t *len) try {
+    if (!h || !len) { set_err("NULL argument"); return PG_EINVAL; }
+    if (!(h->flags & PG_TRACE)) { set_err("pg_get_trace: handle not loaded with PG_TRACE"); return PG_ESTATE; }
+    const int64_t nrec = (int64_t)(h->ptrace.size() / 5);
+    *len = nrec;
+    if (records && cap > 0)
+        std::memcpy(records, h->ptrace.data(), sizeof(uint64_t) * 5 * (size_t)std::min(cap, nrec));
+    return PG_OK;
+} PGSI_ABI_CATCH
+
+pg_status pg_get_stats(pg_game h, pg_stats *stats) try {
     if (!h || !stats) { set_err("NULL argument"); return PG_EINVAL; }
     *stats = h->st;
     return PG_OK;
-}
+} PGSI_ABI_CATCH
 
-pg_status pg_valuate(pg_game h, const int32_t *strategy, int32_t *val, uint8_t *top, int32_t *cycle_dom) {
+pg_status pg_valuate(pg_game h, const int32_t *strategy, int32_t *val, uint8_t *top, int32_t *cycle_dom) try {
     pg_status rc = check_handle(h);
     if (rc) return rc;
     if (!strategy && h->G.n_int) { set_err("NULL strategy"); return PG_EINVAL; }
@@ -1010,10 +1081,10 @@ pg_status pg_valuate(pg_game h, const int32_t *strategy, int32_t *val, uint8_t *
     timing_collect(h);
     h->st.ms_call = now_ms() - t0;
     return PG_OK;
-}
+} PGSI_ABI_CATCH
 
 pg_status pg_best_response(pg_game h, const int32_t *sigma, const int32_t *tau0, int32_t *tau_out,
-                           int32_t *val, uint8_t *top, int64_t *inner_iters) {
+                           int32_t *val, uint8_t *top, int64_t *inner_iters) try {
     pg_status rc = check_handle(h);
     if (rc) return rc;
     if (!sigma && h->G.n_int) { set_err("NULL sigma"); return PG_EINVAL; }
@@ -1043,9 +1114,9 @@ pg_status pg_best_response(pg_game h, const int32_t *sigma, const int32_t *tau0,
     timing_collect(h);
     h->st.ms_call = now_ms() - t0;
     return PG_OK;
-}
+} PGSI_ABI_CATCH
 
-pg_status pg_solve(pg_game h, uint8_t *winner, int32_t *sigma, int32_t *tau, int32_t *val, pg_stats *stats) {
+pg_status pg_solve(pg_game h, uint8_t *winner, int32_t *sigma, int32_t *tau, int32_t *val, pg_stats *stats) try {
     pg_status rc = check_handle(h);
     if (rc) return rc;
     if (!winner && h->n) { set_err("NULL winner"); return PG_EINVAL; }
@@ -1066,7 +1137,8 @@ pg_status pg_solve(pg_game h, uint8_t *winner, int32_t *sigma, int32_t *tau, int
         }
         // the whole of Algorithm 1 in one single-block launch (pg_small.cu) when its state
         // fits in shared memory
-        const bool small = h->G.n_int + 1 <= h->small_max && !h->dist_fn && !(h->flags & PG_BELLMAN_FORD) &&
+        const bool small = h->G.n_int + 1 <= h->small_max && !h->dist_fn &&
+                           !(h->flags & (PG_BELLMAN_FORD | PG_TRACE)) &&
                            small_scratch_bytes(h->G.n_int, h->G.dp, check) <= (size_t)h->smem_optin;
         if (small) {
             {
@@ -1139,6 +1211,6 @@ pg_status pg_solve(pg_game h, uint8_t *winner, int32_t *sigma, int32_t *tau, int
     h->st.ms_call = now_ms() - t0;
     if (stats) *stats = h->st;
     return PG_OK;
-}
+} PGSI_ABI_CATCH
 
 }  // extern "C"

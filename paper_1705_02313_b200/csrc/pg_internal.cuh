@@ -186,6 +186,11 @@ cudaError_t launch_export_winner(const DevGame &g, int64_t count, uint8_t *out, 
 cudaError_t launch_export_cycle_dom(const DevGame &g, int64_t count, const int32_t *D_dev,
                                     int32_t *out, cudaStream_t s);
 cudaError_t setup_launch_cfg(LaunchCfg &lc, int device);
+// per-iteration parity trace (pg_trace.cu): out[0] = h_succ, out[1] = h_val, out[2] = n_top
+// of the profile tsucc and the valuation in top/pidx (L*, J* = (n_int+1)-entry scratch)
+cudaError_t launch_trace_hash(const DevGame &g, int sms, const int32_t *tsucc, unsigned long long *L0,
+                              unsigned long long *L1, int32_t *J0, int32_t *J1, unsigned long long *out,
+                              cudaStream_t s);
 
 // host-side canonical game (pg_load.cpp)
 struct HostGame {

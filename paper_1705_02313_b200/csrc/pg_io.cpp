@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "pg.h"
+#include "pg_guard.h"
 
 namespace pgsi {
 void io_set_err(const std::string &s);   // pg_api.cu (thread-local last error)
@@ -77,6 +78,10 @@ struct Parsed {
 bool parse(const char *text, int64_t len, Parsed &out, std::string &err) {
     Parser p{text, len};
     int64_t maxid = -1;
+    // Every vertex must be defined by a statement of at least 8 bytes ("0 0 0 0;"),
+    // so a valid input has at most len/8 vertices: larger ids are rejected before
+    // anything is sized by them (a short input cannot demand a huge allocation).
+    const int64_t id_limit = len / 8 + 1;
     struct V { int64_t pri; int owner; std::vector<int64_t> succ; bool seen = false; };
     std::vector<V> vs;
     auto get = [&](int64_t id) -> V & {
@@ -87,6 +92,11 @@ bool parse(const char *text, int64_t len, Parsed &out, std::string &err) {
     if (p.word("parity")) {
         if (!p.num(maxid)) { err = p.err; return false; }
         if (maxid >= (int64_t)INT32_MAX - 1) { p.fail("maxid too large"); err = p.err; return false; }
+        if (maxid >= id_limit) {
+            p.fail("maxid " + std::to_string(maxid) + " needs more vertex statements than the input can hold");
+            err = p.err;
+            return false;
+        }
         vs.reserve((size_t)maxid + 1);
         p.ws();
         if (!p.word(";")) { p.fail("expected ';' after the parity header"); err = p.err; return false; }
@@ -107,6 +117,11 @@ bool parse(const char *text, int64_t len, Parsed &out, std::string &err) {
         if (pr > INT32_MAX) { p.fail("priority too large"); err = p.err; return false; }
         if (maxid >= 0 && id > maxid) { p.fail("vertex id " + std::to_string(id) + " exceeds the header's maxid"); err = p.err; return false; }
         if (id >= (int64_t)INT32_MAX - 1) { p.fail("vertex id " + std::to_string(id) + " too large"); err = p.err; return false; }
+        if (id >= id_limit) {
+            p.fail("vertex id " + std::to_string(id) + " exceeds the number of vertex statements the input can hold");
+            err = p.err;
+            return false;
+        }
         V &v = get(id);
         if (v.seen) { p.fail("duplicate definition of vertex " + std::to_string(id)); err = p.err; return false; }
         v.seen = true;
@@ -224,10 +239,24 @@ int64_t cycle_through(const std::vector<int64_t> &verts, const std::vector<int64
 
 }  // namespace
 
+namespace pgsi {
+// CSR sanity of a game passed to a verifier: row_ptr[0] = 0, every vertex has an
+// out-edge, successors in [0, n). Returns the first bad vertex or -1.
+int64_t csr_check(int64_t n, const int64_t *row_ptr, const int32_t *col, std::string &why) {
+    if (n > 0 && row_ptr[0] != 0) { why = "row_ptr[0] != 0"; return 0; }
+    for (int64_t v = 0; v < n; v++) {
+        if (row_ptr[v + 1] <= row_ptr[v]) { why = "terminal vertex or decreasing row_ptr"; return v; }
+        for (int64_t e = row_ptr[v]; e < row_ptr[v + 1]; e++)
+            if (col[e] < 0 || col[e] >= n) { why = "successor " + std::to_string(col[e]) + " out of range"; return v; }
+    }
+    return -1;
+}
+}  // namespace pgsi
+
 extern "C" {
 
 pg_status pg_parse_pgsolver(const char *text, int64_t len, int64_t *n, int64_t *m, int64_t *row_ptr,
-                            int32_t *col, uint8_t *owner, int32_t *priority) {
+                            int32_t *col, uint8_t *owner, int32_t *priority) try {
     if (!text && len) { pgsi::io_set_err("NULL text"); return PG_EINVAL; }
     Parsed P;
     std::string err;
@@ -239,10 +268,10 @@ pg_status pg_parse_pgsolver(const char *text, int64_t len, int64_t *n, int64_t *
     if (owner && P.n) memcpy(owner, P.owner.data(), (size_t)P.n);
     if (priority && P.n) memcpy(priority, P.pri.data(), sizeof(int32_t) * (size_t)P.n);
     return PG_OK;
-}
+} PGSI_ABI_CATCH
 
 pg_status pg_format_solution(int64_t n, const uint8_t *owner, const uint8_t *winner, const int32_t *sigma,
-                             const int32_t *tau, char *buf, int64_t cap, int64_t *len) {
+                             const int32_t *tau, char *buf, int64_t cap, int64_t *len) try {
     if (n < 0 || (n && (!owner || !winner || !sigma || !tau))) { pgsi::io_set_err("NULL argument"); return PG_EINVAL; }
     std::string s = "paritysol " + std::to_string(n - 1) + ";\n";
     for (int64_t v = 0; v < n; v++) {
@@ -259,11 +288,11 @@ pg_status pg_format_solution(int64_t n, const uint8_t *owner, const uint8_t *win
         memcpy(buf, s.c_str(), s.size() + 1);
     }
     return PG_OK;
-}
+} PGSI_ABI_CATCH
 
 pg_status pg_verify_solution(int64_t n, const int64_t *row_ptr, const int32_t *col, const uint8_t *owner,
                              const int32_t *priority, const uint8_t *winner, const int32_t *sigma,
-                             const int32_t *tau, int64_t *witness) {
+                             const int32_t *tau, int64_t *witness) try {
     if (witness) *witness = -1;
     if (n < 0 || (n && (!row_ptr || !col || !owner || !priority || !winner || !sigma || !tau))) {
         pgsi::io_set_err("NULL argument");
@@ -274,10 +303,13 @@ pg_status pg_verify_solution(int64_t n, const int64_t *row_ptr, const int32_t *c
         pgsi::io_set_err("solution rejected at vertex " + std::to_string(v) + ": " + why);
         return PG_EINVAL;
     };
-    for (int64_t v = 0; v < n; v++) {
-        if (row_ptr[v + 1] <= row_ptr[v]) return bad(v, "terminal vertex in the game");
-        if (winner[v] > 1) return bad(v, "winner must be 0 or 1");
+    {
+        std::string why;
+        const int64_t v = pgsi::csr_check(n, row_ptr, col, why);
+        if (v >= 0) return bad(v, "malformed game: " + why);
     }
+    for (int64_t v = 0; v < n; v++)
+        if (winner[v] > 1) return bad(v, "winner must be 0 or 1");
     // strategy edges (winner's own vertices) and closure
     for (int64_t v = 0; v < n; v++) {
         const int i = winner[v];
@@ -285,7 +317,7 @@ pg_status pg_verify_solution(int64_t n, const int64_t *row_ptr, const int32_t *c
             const int32_t x = i == 0 ? sigma[v] : tau[v];
             bool edge = false;
             for (int64_t e = row_ptr[v]; e < row_ptr[v + 1]; e++) edge |= col[e] == x;
-            if (!edge) return bad(v, "strategy choice " + std::to_string(x) + " is not an edge");
+            if (!edge || x < 0 || x >= n) return bad(v, "strategy choice " + std::to_string(x) + " is not an edge");
             if (winner[x] != i) return bad(v, "strategy edge leaves the winning set");
         } else {
             for (int64_t e = row_ptr[v]; e < row_ptr[v + 1]; e++)
@@ -327,6 +359,6 @@ pg_status pg_verify_solution(int64_t n, const int64_t *row_ptr, const int32_t *c
         }
     }
     return PG_OK;
-}
+} PGSI_ABI_CATCH
 
 }  // extern "C"

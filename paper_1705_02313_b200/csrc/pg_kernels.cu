@@ -1217,6 +1217,12 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
     if (blockIdx.x == 0 && threadIdx.x == 0) { ctl->nswl = 0; ctl->nhard = 0; }  // step 5 appends anew
     int64_t lo = 0, hi = ns;
     int levels = 0;
+    // The per-level append counters rotate on the count of GRID levels (glev), which
+    // the block-0 thin-frontier mode below never advances and never touches: a block
+    // released late from the last grid level's barrier may still be reading
+    // dcnt[glev % 3] while block 0 runs thin levels, and the grid resumes on the next
+    // counter of the rotation, which is zero (reset two grid levels ahead).
+    int glev = 0;
     while (lo < hi && levels < (1 << 30)) {
         if (gridDim.x > 1 && hi - lo <= g.inc_blk_frontier) {
             // Thin frontier (the long chains of a deep closure): block 0 runs the
@@ -1253,7 +1259,6 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
                     ctl->blk[1] = (unsigned long long)bhi;
                     ctl->blk[2] = (unsigned long long)blev;
                     ctl->blk[3] = abort ? 1ull : 0ull;
-                    ctl->dcnt[0] = ctl->dcnt[1] = ctl->dcnt[2] = 0;
                     if (abort) { ctl->inc_overflow = 1; ctl->nD = (unsigned long long)bhi; }
                 }
             }
@@ -1265,8 +1270,9 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
             continue;
         }
         levels++;
-        unsigned long long *cnt = &ctl->dcnt[levels % 3];   // reset two levels ahead: no block
-        int32_t *out = g.Dl + hi;                           // reads a count still being written
+        glev++;
+        unsigned long long *cnt = &ctl->dcnt[glev % 3];     // reset two grid levels ahead: no
+        int32_t *out = g.Dl + hi;                           // block reads a count still being written
         for (int64_t b0 = lo + wbase; b0 < hi; b0 += stride) {
             const int64_t i = b0 + lane;
             int32_t f = -1;
@@ -1279,7 +1285,7 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
         }
         gbar(ctl);
         const int64_t added = (int64_t)bcast_ld(cnt);
-        if (blockIdx.x == 0 && threadIdx.x == 0) ctl->dcnt[(levels + 2) % 3] = 0;
+        if (blockIdx.x == 0 && threadIdx.x == 0) ctl->dcnt[(glev + 2) % 3] = 0;
         lo = hi;
         hi += added;
         if (levels >= g.inc_max_levels || hi > g.inc_max_dirty) {
@@ -1926,8 +1932,7 @@ cudaError_t launch_even_inc(const DevGame &g, cudaStream_t s) {
 }
 
 cudaError_t launch_inc_iter(const DevGame &g, const LaunchCfg &lc, cudaStream_t s, int64_t nS) {
-    static const int64_t mul = getenv("PGSI_INC_GRID_MUL") ? atoi(getenv("PGSI_INC_GRID_MUL")) : 16;
-    int64_t grid = (nS * mul + kThreads - 1) / kThreads;
+    int64_t grid = (nS * (int64_t)g.inc_grid_mul + kThreads - 1) / kThreads;   // as k_inc_iter's step 8 rule
     grid = std::max<int64_t>(1, std::min<int64_t>(grid, lc.coop_inc));
     DevGame gg = g;
     void *args[] = {&gg};

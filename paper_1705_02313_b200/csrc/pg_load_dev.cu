@@ -24,10 +24,11 @@ namespace pgsi {
 namespace {
 
 constexpr int T = 256;
+int g_sms = 148;   // SM count of the loading device (build_device_game queries it)
 
 inline int grid1(int64_t n) {
     int64_t b = (n + T - 1) / T;
-    return (int)std::max<int64_t>(1, std::min<int64_t>(b, 148 * 32));
+    return (int)std::max<int64_t>(1, std::min<int64_t>(b, (int64_t)g_sms * 32));
 }
 
 #define GS_LOOP(i, n) for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < (n); \
@@ -264,6 +265,12 @@ pg_status build_device_game(int64_t n, const int64_t *row_ptr, const int32_t *co
     if (n < 0) { err = "n < 0"; return PG_EINVAL; }
     if (n > 0 && (!row_ptr || !col || !owner || !priority)) { err = "NULL input array"; return PG_EINVAL; }
     if (n >= (int64_t(1) << 31) - 2) { err = "more than 2^31-3 vertices"; return PG_ENOTSUP; }
+    {
+        int dev = 0, sms = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess &&
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess && sms > 0)
+            g_sms = sms;
+    }
     if (n > 0 && row_ptr[0] != 0) { err = "row_ptr[0] != 0"; return PG_EINVAL; }
     const int64_t m = n ? row_ptr[n] : 0;
     if (m < 0 || m >= (int64_t(1) << 31)) { err = "row_ptr[n] out of range"; return PG_ENOTSUP; }

@@ -36,9 +36,11 @@
 #include <vector>
 
 #include "pg.h"
+#include "pg_guard.h"
 
 namespace pgsi {
 void io_set_err(const std::string &s);   // pg_api.cu
+int64_t csr_check(int64_t n, const int64_t *row_ptr, const int32_t *col, std::string &why);   // pg_io.cpp
 }
 
 namespace {
@@ -165,7 +167,7 @@ struct DevBuf {
 extern "C" pg_status pg_verify_solution_device(int64_t n, const int64_t *row_ptr, const int32_t *col,
                                                const uint8_t *owner, const int32_t *priority,
                                                const uint8_t *winner, const int32_t *sigma, const int32_t *tau,
-                                               int32_t device, int64_t *witness, int64_t *rounds_out) {
+                                               int32_t device, int64_t *witness, int64_t *rounds_out) try {
     if (witness) *witness = -1;
     if (rounds_out) *rounds_out = 0;
     if (n < 0 || (n && (!row_ptr || !col || !owner || !priority || !winner || !sigma || !tau))) {
@@ -174,6 +176,15 @@ extern "C" pg_status pg_verify_solution_device(int64_t n, const int64_t *row_ptr
     }
     if (n == 0) return PG_OK;
     if (n >= (int64_t(1) << 31) - 1) { pgsi::io_set_err("too many vertices"); return PG_ENOTSUP; }
+    {
+        std::string why;
+        const int64_t v = pgsi::csr_check(n, row_ptr, col, why);
+        if (v >= 0) {
+            if (witness) *witness = v;
+            pgsi::io_set_err("solution rejected at vertex " + std::to_string(v) + ": malformed game: " + why);
+            return PG_EINVAL;
+        }
+    }
     // host: priority indices (D sorted), the winner's own choice per vertex, basic range checks
     std::vector<int32_t> D(priority, priority + n);
     std::sort(D.begin(), D.end());
@@ -276,4 +287,4 @@ extern "C" pg_status pg_verify_solution_device(int64_t n, const int64_t *row_ptr
     }
     if (prev != device) cudaSetDevice(prev);
     return rc;
-}
+} PGSI_ABI_CATCH

@@ -30,6 +30,7 @@ PG_HOST_LOAD = 32
 PG_BFS = 64
 PG_SI_RESET = 128
 PG_BELLMAN_FORD = 256
+PG_TRACE = 512
 BEST_RESPONSE = {"si": 0, "si_reset": PG_SI_RESET, "bf": PG_BELLMAN_FORD}
 
 STATUS = {0: "PG_OK", -1: "PG_EINVAL", -2: "PG_ENOMEM", -3: "PG_ECUDA", -4: "PG_ENCCL",
@@ -93,10 +94,11 @@ def load_library(path: str = LIB_PATH):
     L.pg_best_response.argtypes = [C.c_void_p, P, P, P, P, P, P]
     L.pg_solve.argtypes = [C.c_void_p, P, P, P, P, C.POINTER(Stats)]
     L.pg_get_stats.argtypes = [C.c_void_p, C.POINTER(Stats)]
+    L.pg_get_trace.argtypes = [C.c_void_p, P, C.c_int64, P]
     L.pg_inspect.argtypes = [C.c_int64, P, P, P, P, C.c_uint32] + [P] * 9
     L.pg_dist_attach.argtypes = [C.c_void_p, C.c_int32, C.c_int32, ALLGATHER_FN, P]
     for f in ("pg_load", "pg_info", "pg_valuate", "pg_best_response", "pg_solve", "pg_get_stats",
-              "pg_inspect", "pg_dist_attach"):
+              "pg_inspect", "pg_dist_attach", "pg_get_trace"):
         getattr(L, f).restype = C.c_int
     L.pg_parse_pgsolver.argtypes = [C.c_char_p, C.c_int64, P, P, P, P, P, P]
     L.pg_format_solution.argtypes = [C.c_int64, P, P, P, P, C.c_char_p, C.c_int64, P]
@@ -136,16 +138,18 @@ class Game:
                  preprocess: bool = True, check: bool = False, phase_timing: bool = False,
                  device_ptrs: bool = False, splitter_k: int = 0, max_inner: int = 0,
                  max_outer: int = 0, prefix_pairs: int = 0, incremental: bool = True,
-                 host_load: bool = False, bfs: bool = False, best_response: str = "si"):
+                 host_load: bool = False, bfs: bool = False, best_response: str = "si",
+                 trace: bool = False):
         """best_response: "si" (Algorithm 1), "si_reset" (PG_SI_RESET) or "bf"
-        (PG_BELLMAN_FORD), the arms of the paper's Table 2."""
+        (PG_BELLMAN_FORD), the arms of the paper's Table 2.
+        trace: record the per-iteration parity trace (PG_TRACE; ``get_trace``)."""
         L = load_library()
         self._in = (np.ascontiguousarray(row_ptr, np.int64), np.ascontiguousarray(col, np.int32),
                     np.ascontiguousarray(owner, np.uint8), np.ascontiguousarray(priority, np.int32))
         flags = ((0 if preprocess else PG_NO_PREPROCESS) | (PG_CHECK_INVARIANTS if check else 0) |
                  (PG_PHASE_TIMING if phase_timing else 0) | (PG_PTRS_ON_DEVICE if device_ptrs else 0) |
                  (0 if incremental else PG_NO_INCREMENTAL) | (PG_HOST_LOAD if host_load else 0) |
-                 (PG_BFS if bfs else 0) | BEST_RESPONSE[best_response])
+                 (PG_BFS if bfs else 0) | BEST_RESPONSE[best_response] | (PG_TRACE if trace else 0))
         opt = Options(flags, device, C.c_void_p(stream) if stream else None, splitter_k,
                       prefix_pairs, max_inner, max_outer)
         h = C.c_void_p()
@@ -221,6 +225,15 @@ class Game:
         s = Stats()
         self._check(_lib.pg_get_stats(self._h, C.byref(s)))
         return s.as_dict()
+
+    def get_trace(self) -> np.ndarray:
+        """Per-iteration parity trace of the last solve / best response (``pg_get_trace``):
+        uint64 [records, 5] rows (kind, h_succ, h_val, n_top, switches)."""
+        n = C.c_int64()
+        self._check(_lib.pg_get_trace(self._h, None, 0, C.byref(n)))
+        rec = np.zeros((max(n.value, 1), 5), np.uint64)
+        self._check(_lib.pg_get_trace(self._h, _ptr(rec), n.value, C.byref(n)))
+        return rec[:n.value]
 
     def valuate(self, strategy, want_cycle_dom: bool = True):
         N, d = self.n_internal, self.d

@@ -144,3 +144,33 @@ def test_verify_rejects_escaping_and_non_edges(pg):
     ok, w, msg = pg.verify_solution(g, np.array([0, 1], np.uint8), np.array([1, -2], np.int32),
                                     np.array([-2, 1], np.int32))
     assert not ok and w == 0 and "leaves the winning set" in msg
+
+
+@pytest.mark.parametrize("txt", ["2000000000 0 0 0;", "parity 2000000000; 0 0 0 0;",
+                                 "parity 5; 0 0 0 0;", "300 1 0 1;"])
+def test_parse_rejects_ids_the_input_cannot_define(pg, txt):
+    """A vertex id (or header maxid) larger than the number of vertex statements the
+    input can hold (each is >= 8 bytes) is an error before any allocation sized by
+    it: a short input must not abort the process."""
+    with pytest.raises(pg.PGError) as e:
+        pg.parse_pgsolver(txt)
+    assert e.value.name == "PG_EINVAL"
+
+
+@pytest.mark.parametrize("bad", ["col_range", "col_neg", "row_ptr0", "terminal"])
+def test_verify_rejects_malformed_csr(pg, bad):
+    """Both verifiers check the CSR before indexing winner[col[e]]."""
+    g = gi.random_game(50, 3, 1, 3, 1)
+    r = Oracle(g).solve()
+    rp, col = g.row_ptr.copy(), g.col.copy()
+    if bad == "col_range":
+        col[7] = 10_000_000
+    elif bad == "col_neg":
+        col[3] = -5
+    elif bad == "row_ptr0":
+        rp = rp + 1
+    else:
+        rp[5] = rp[4]
+    gb = gi.Game(rp, col, g.owner, g.priority)
+    ok, w, msg = pg.verify_solution(gb, r.winner, r.sigma, r.tau)
+    assert not ok and "malformed game" in msg
