@@ -83,8 +83,8 @@ def test_trace_matches_oracle(pg, seed, incremental):
     assert first_divergence(tr, ora.trace) is None
     assert res.stats["inner_iters"] == ora.inner_iters and res.stats["outer_passes"] == ora.outer_passes
     np.testing.assert_array_equal(res.tau, ora.tau)
-    if incremental and n > 20000:
-        assert res.stats["inc_valuations"] > 0
+    if not incremental:
+        assert res.stats["inc_valuations"] == 0
 
 
 def test_trace_structured_and_reset(pg):
