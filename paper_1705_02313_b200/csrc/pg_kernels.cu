@@ -5,16 +5,22 @@
 //                       jumping on packed (J, len) words
 //   V2  k_spl_*         (only when some play is deeper than K) depth-strided
 //                       splitters + Wyllie over the reduced forest's d-vector rows
-//       k_v2_walk       d-vector path counts: each lane walks its
-//                       vertex's play to the sink or the nearest splitter with a
-//                       byte-packed register histogram, then the warp writes the
-//                       32 rows as coalesced row stores (the list-ranking step of
-//                       PAPER.md:613-653, re-designed)
+//       k_v2_cpx        d-vector path counts: each thread walks its
+//                       vertex's play (two steps per dependent load) to the sink or
+//                       the nearest splitter, counting priorities in a byte
+//                       histogram, and merges them into the exit vertex's 32-byte
+//                       compact prefix (the list-ranking step of PAPER.md:613-653,
+//                       re-designed). k_v2_rows writes full rows
+//                       for outputs only.
 //   S   k_switch<ODD>   All_Odd / All_Even
-//                       (PAPER.md:416-434, 487-491): a group of dp lanes per vertex,
-//                       one key column per lane, lexicographic compare by two warp
-//                       ballots; switch counts by ballot+popc, one atomic per block
+//                       (PAPER.md:416-434, 487-491): one thread per vertex scans its
+//                       candidates in canonical order, in batches of 6 independent
+//                       loads, comparing 8-byte switch keys (then 32-byte compact
+//                       prefixes, then a deferred hard pass that re-walks plays);
+//                       switch counts block-reduced, one atomic per block
 //                       (convergence test, Algorithm 1 "until S = ∅").
+//   inc k_inc_iter      incremental valuation + All_Odd over E,
+//                       several inner iterations per cooperative launch.
 #include <cooperative_groups.h>
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
@@ -856,13 +862,13 @@ __device__ __noinline__ int cmp_full(const DevGame &g, int32_t a, int32_t b) {
         while (dx > dy) {
             const uint32_t p = (uint32_t)__ldg(g.pidx + x) - 32u * c;
             if (p < 32u) ca[p]++;
-            x = __ldg(g.succ + x);
+            x = __ldcg(g.succ + x);
             dx--;
         }
         while (dy > dx) {
             const uint32_t p = (uint32_t)__ldg(g.pidx + y) - 32u * c;
             if (p < 32u) cb[p]++;
-            y = __ldg(g.succ + y);
+            y = __ldcg(g.succ + y);
             dy--;
         }
         while (x != y && dx > 0) {
@@ -870,8 +876,8 @@ __device__ __noinline__ int cmp_full(const DevGame &g, int32_t a, int32_t b) {
             const uint32_t q = (uint32_t)__ldg(g.pidx + y) - 32u * c;
             if (p < 32u) ca[p]++;
             if (q < 32u) cb[q]++;
-            x = __ldg(g.succ + x);
-            y = __ldg(g.succ + y);
+            x = __ldcg(g.succ + x);
+            y = __ldcg(g.succ + y);
             dx--;
         }
         for (int col = min(32 * c + 31, g.dp - 1); col >= 32 * c; col--) {
@@ -905,11 +911,13 @@ __device__ __forceinline__ int cmp_key(uint2 a, uint2 b) {
 
 // ⊑ of val(a), val(b) from their 32-byte prefixes (after an undecided key
 // compare); HARD: resolve an undecided prefix compare by re-walking the plays.
+// succ, key and cpx are read with ld.global.cg (L2), never through the read-only
+// path: k_inc_iter rewrites them between the steps of one launch.
 template <bool HARD>
 __device__ __forceinline__ int cmp_pref(const DevGame &g, const uint4 *cpx, int32_t a, int32_t b,
                                         unsigned long long &pref, unsigned long long &fulls) {
-    const uint4 a0 = __ldg(cpx + 2 * (int64_t)a), a1 = __ldg(cpx + 2 * (int64_t)a + 1);
-    const uint4 b0 = __ldg(cpx + 2 * (int64_t)b), b1 = __ldg(cpx + 2 * (int64_t)b + 1);
+    const uint4 a0 = __ldcg(cpx + 2 * (int64_t)a), a1 = __ldcg(cpx + 2 * (int64_t)a + 1);
+    const uint4 b0 = __ldcg(cpx + 2 * (int64_t)b), b1 = __ldcg(cpx + 2 * (int64_t)b + 1);
     pref += 2;
     const uint32_t wa[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
     const uint32_t wb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
@@ -930,7 +938,7 @@ __device__ __forceinline__ int switch_vertex(const DevGame &g, int64_t v, const 
                                              unsigned long long &pref) {
     constexpr int B = 6;   // one batch for out-degree <= 5 plus the sink (measured: 4 -> 6 saves 1.1 ms per config-3 solve)
     const int32_t SINK = (int32_t)g.n_int;
-    const int32_t cur = __ldg(g.succ + v);
+    const int32_t cur = __ldcg(g.succ + v);
     const uint32_t beg = __ldg(g.rp + v), end = __ldg(g.rp + v + 1);
     const int32_t ncand = (int32_t)(end - beg) + (ODD ? 0 : 1);
     int32_t best = -1;
@@ -948,7 +956,7 @@ __device__ __forceinline__ int switch_vertex(const DevGame &g, int64_t v, const 
         for (int k = 0; k < B; k++) {
             kk[k] = make_uint2(0u, 0u);
             if (c[k] >= 0) {
-                kk[k] = __ldg(g.key + c[k]);
+                kk[k] = __ldcg(g.key + c[k]);
                 reads += (c[k] != SINK);
             }
         }
@@ -1230,13 +1238,16 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
             // a counter read, while the frontier stays thin; the grid resumes if it
             // widens. Same expansion, same lists; only the synchronisation differs.
             if (blockIdx.x == 0) {
-                __shared__ unsigned long long bcnt;
+                // the level counter alternates between two words: thread 0 zeroes the
+                // next one while slower threads may still read this level's (racecheck)
+                __shared__ unsigned long long bcnt[2];
                 int64_t blo = lo, bhi = hi;
                 int blev = levels;
                 bool abort = false;
                 while (blo < bhi && bhi - blo <= 4 * (int64_t)g.inc_blk_frontier) {
                     blev++;
-                    if (threadIdx.x == 0) bcnt = 0;
+                    unsigned long long *bc = &bcnt[blev & 1];
+                    if (threadIdx.x == 0) *bc = 0;
                     __syncthreads();
                     int32_t *out = g.Dl + bhi;
                     for (int64_t b0 = blo + (threadIdx.x - lane); b0 < bhi; b0 += blockDim.x) {
@@ -1247,11 +1258,11 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
                             f = __ldcg(g.Dl + i);
                             r = __ldcg(g.Dr + i);
                         }
-                        expand_closure(g, f, r.x, r.y, ep, out, g.Dr + bhi, &bcnt);
+                        expand_closure(g, f, r.x, r.y, ep, out, g.Dr + bhi, bc);
                     }
                     __syncthreads();
                     blo = bhi;
-                    bhi += (int64_t)bcnt;
+                    bhi += (int64_t)*bc;
                     if (blev >= g.inc_max_levels || bhi > g.inc_max_dirty) { abort = true; break; }
                 }
                 if (threadIdx.x == 0) {
@@ -1394,7 +1405,7 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
                 int32_t x = v;
                 while (x != (int32_t)N && __ldcg(g.dmark + x) == ep) {
                     const uint32_t p = __ldg(g.pidx + x);
-                    x = __ldg(g.succ + x);
+                    x = __ldcg(g.succ + x);
                     if (++hb[p] == 255) { atomicOr(&ctl->inc_overflow, 1ull); break; }
                     mask |= 1u << p;
                     steps++;
