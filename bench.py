@@ -52,6 +52,9 @@ WORKLOADS = {
                  desc="F_deep(4M) closed-form family: one 4M-deep finite play, d=3 (BASELINE configs[3])"),
     "stair": dict(family="stair", L=5000, ref_iters=200, cpu_iters=400,
                   desc="F_stair(5000) long-iteration family: 5000 outer passes (BASELINE configs[4])"),
+    "stair20k": dict(family="stair", L=20000, ref_iters=100, cpu_iters=200,
+                     desc="F_stair(20000) long-iteration family: 20000 outer passes, too large for the "
+                          "single-block kernel (BASELINE configs[4])"),
 }
 THROTTLE_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
                  0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
@@ -255,8 +258,9 @@ def main():
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
     game = make_game(wl, pgdist.game_seed(args.seed, rank))   # weak scaling: an independent game per rank
-    G = Game.from_game(game, device=local, stream=stream.cuda_stream, device_ptrs=True,
-                       phase_timing=True)
+    # timed solves: the default path (Algorithm 1 as one CUDA graph launch per solve for
+    # large games, pg_loop.cu; one single-block kernel for small ones)
+    G = Game.from_game(game, device=local, stream=stream.cuda_stream, device_ptrs=True)
     n = game.n
     out = (torch.empty(n, dtype=torch.uint8, device=dev), torch.empty(n, dtype=torch.int32, device=dev),
            torch.empty(n, dtype=torch.int32, device=dev), None)
@@ -275,7 +279,7 @@ def main():
                             "n_even", "n_inc", "gpu_launches", "inner_iters", "outer_passes",
                             "full_compares", "v1_rounds", "v2_split_valuations", "inc_valuations",
                             "dirty_vertices", "ms_bfs", "n_bfs", "bytes_bfs", "bfs_valuations",
-                            "prefix_gathers")}
+                            "prefix_gathers", "device_loop_solves", "small_solves")}
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     barrier()
@@ -293,6 +297,26 @@ def main():
     value = units / (ms / 1000.0)
     inner = int(acc["inner_iters"] / args.steps)
     outer = int(acc["outer_passes"] / args.steps)
+    timed_stats = dict(acc)
+
+    # ---- per-phase CUDA events (PG_PHASE_TIMING): kernel times for the roofline block.
+    # Events around every phase need the host-driven loop, so these are separate solves of
+    # the same game right after the timed region (same kernels, same launch sequence).
+    Gp = Game.from_game(game, device=local, stream=stream.cuda_stream, device_ptrs=True, phase_timing=True)
+    Gp.solve(out=out)
+    acc = {k: 0.0 for k in acc}
+    torch.cuda.synchronize(dev)
+    ep0 = torch.cuda.Event(enable_timing=True)
+    ep1 = torch.cuda.Event(enable_timing=True)
+    ep0.record(stream)
+    for _ in range(args.steps):
+        r = Gp.solve(out=out)
+        for k in acc:
+            acc[k] += r.stats[k]
+    ep1.record(stream)
+    torch.cuda.synchronize(dev)
+    host_loop_ms = ep0.elapsed_time(ep1) / args.steps
+    Gp.free()
 
     # ---- roofline of the dominant kernel (phase with the largest event time)
     peak, peak_src = measured_peak_gbs()
@@ -313,6 +337,9 @@ def main():
                 "bytes_per_launch": dbytes / max(dn, 1), "ms_per_launch": dms / max(dn, 1),
                 "share_of_step": dms / total_phase_ms if total_phase_ms else None,
                 "peak_source": peak_src,
+                "timing": "CUDA events around each phase on the library's stream, over the same number "
+                          "of solves of this game with PG_PHASE_TIMING (host-driven loop) right after "
+                          f"the timed region ({host_loop_ms:.2f} ms per solve that way)",
                 "phases": {p: {"ms_per_launch": v[0] / max(v[2], 1),
                                "GBps": (v[1] / (v[0] / 1000.0) / 1e9) if v[0] else None,
                                "launches": int(v[2] / args.steps)} for p, v in phases.items()}}
@@ -442,6 +469,10 @@ def main():
                        "split_valuations_per_solve": int(acc["v2_split_valuations"] / args.steps),
                        "incremental_valuations_per_solve": int(acc["inc_valuations"] / args.steps),
                        "mean_dirty_fraction": (acc["dirty_vertices"] / max(acc["inc_valuations"], 1)) / G.n_internal,
+                       "loop": ("device: one CUDA graph launch per solve (conditional WHILE/SWITCH nodes)"
+                                if timed_stats["device_loop_solves"] else
+                                "single-block whole-solve kernel" if timed_stats["small_solves"] else "host-driven"),
+                       "host_loop_ms_per_solve": host_loop_ms,
                        "parallelism": "single GPU" if world == 1 else f"weak: {world} independent games",
                        "l2": f"inputs larger than L2: per-iteration working set {ws_bytes / 1e9:.2f} GB "
                              f"(prefixes, jl, succ, pidx, ⊤, CSR) > 126 MB; no flush needed"},
@@ -452,7 +483,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "clocks": sampler.summary(),
-            "gpu_launches": int(acc["gpu_launches"]),
+            "gpu_launches": int(timed_stats["gpu_launches"]),
         }
         print(json.dumps(line), flush=True)
     G.free()

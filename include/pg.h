@@ -170,6 +170,10 @@ typedef struct {
     int64_t bf_rounds;       /* relaxation rounds (= inner_iters of a BF solve)             */
     double ms_bf;            /* PG_PHASE_TIMING: CUDA-event total of the rounds             */
     int64_t n_bf;
+    int64_t device_loop_solves; /* pg_solve calls whose whole Algorithm 1 ran as one CUDA
+                                graph with conditional nodes (pg_loop.cu): no host round
+                                trip per iteration; per-phase times and bytes_odd/even/inc
+                                need PG_PHASE_TIMING, which uses the host-driven loop    */
     double bytes_bf;         /* algorithmic bytes of the rounds: per vertex pidx (1 B) and
                                 CSR offset / σ (4 B), per Odd edge its target (4 B), τ write
                                 (4 B per Odd vertex), and R = 4·dp bytes per row gathered

@@ -6,7 +6,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpgsi.so")
-SOURCES = ["pg_api.cu", "pg_kernels.cu", "pg_bf.cu", "pg_small.cu", "pg_verify.cu", "pg_trace.cu", "pg_load_dev.cu", "pg_load.cpp", "pg_io.cpp"]
+SOURCES = ["pg_api.cu", "pg_kernels.cu", "pg_bf.cu", "pg_small.cu", "pg_verify.cu", "pg_trace.cu", "pg_loop.cu", "pg_load_dev.cu", "pg_load.cpp", "pg_io.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

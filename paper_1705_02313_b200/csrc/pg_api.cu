@@ -81,6 +81,11 @@ struct pg_game_s {
     unsigned long long *tL[2] = {nullptr, nullptr};
     int32_t *tJ[2] = {nullptr, nullptr};
     unsigned long long *tout = nullptr;       // device h_succ, h_val, n_top
+    // device-resident Algorithm 1 (pg_loop.cu): the instantiated graph and its capture stream
+    cudaGraphExec_t loop_exec = nullptr;
+    cudaStream_t cap_stream = nullptr;
+    bool device_loop = true;                  // PGSI_DEVICE_LOOP=0: the host-driven loop
+    int loop_nodes = 0;
 };
 
 #define CK(h, x)                                                                         \
@@ -247,10 +252,10 @@ pg_status valuate_dev(pg_game h, bool want_cdom, bool full_rows, bool inc = fals
             CK(h, cudaMemsetAsync(h->G.emark, 0, sizeof(uint32_t) * ((size_t)h->G.n_int + 1), h->stream));
             h->epoch = 0;
         }
-        h->G.epoch = h->epoch + 1;
+        CK(h, launch_set_launch_params(h->G.ctl, h->epoch + 1, h->cepoch, h->last_sw_odd ? 1u : 0u, steps,
+                                       h->stream));
         h->epoch += steps;
-        h->G.inc_max_steps = (int32_t)steps;
-        h->G.inc_s_odd = h->last_sw_odd ? 1 : 0;
+        h->st.gpu_launches += 1;
         PhaseScope ps(h, PH_INC);
         CK(h, launch_inc_iter(h->G, h->lc, h->stream, h->last_nsw));
         h->st.gpu_launches += 1;
@@ -490,6 +495,20 @@ pg_status valuate_and_switch(pg_game h, bool odd, bool want_cdom, bool do_switch
                 now_ms() - t_start, (int)inc, inc ? h->h_ctl->steps_done : 1ull, inc ? h->h_ctl->nD_sum : 0ull,
                 h->h_ctl->dlevels, h->h_ctl->v1_rounds, h->h_ctl->walk_steps,
                 inc ? h->h_ctl->nE_sum : h->h_ctl->nE, h->h_ctl->nswl, h->h_ctl->nhard);
+    if (h->trace && inc && h->G.lvlog) {   // PGSI_TRACE=3: the closure's levels of this step
+        std::vector<unsigned long long> lg(8192);
+        CK(h, cudaMemcpy(lg.data(), h->G.lvlog, sizeof(unsigned long long) * 8192, cudaMemcpyDeviceToHost));
+        const unsigned long long cnt = std::min<unsigned long long>(lg[0], 4095);
+        fprintf(stderr, "[pgsi]   closure levels (width/us, * = block 0):");
+        unsigned long long prev = h->h_ctl->ts[0];
+        for (unsigned long long k = 0; k < cnt; k++) {
+            const unsigned long long w = lg[2 + 2 * k], t = lg[3 + 2 * k];
+            fprintf(stderr, " %llu%s/%.1f", w & 0xffffffffull, (w >> 63) ? "*" : "", (t - prev) * 1e-3);
+            prev = t;
+        }
+        fprintf(stderr, "\n");
+        CK(h, cudaMemset(h->G.lvlog, 0, 8));
+    }
     if (h->trace && inc && h->G.trace_ts) {
         const unsigned long long *t = h->h_ctl->ts;
         fprintf(stderr, "[pgsi]   inc phases (us): closure %.1f  C %.1f  V1 %.1f  V2 %.1f  E %.1f  switch %.1f  hard %.1f  apply %.1f\n",
@@ -618,12 +637,13 @@ pg_status even_switch(pg_game h, int64_t *count) {
     {
         PhaseScope ps(h, PH_EVEN);
         if (inc) {
-            h->G.epoch = ++h->epoch;                 // fresh E marks
-            if (h->G.epoch == 0) {
+            if (++h->epoch == 0) {                   // fresh E marks (wrap: clear)
                 CK(h, cudaMemsetAsync(h->G.dmark, 0, sizeof(uint32_t) * ((size_t)h->G.n_int + 1), h->stream));
                 CK(h, cudaMemsetAsync(h->G.emark, 0, sizeof(uint32_t) * ((size_t)h->G.n_int + 1), h->stream));
-                h->G.epoch = ++h->epoch;
+                ++h->epoch;
             }
+            CK(h, launch_set_launch_params(h->G.ctl, h->epoch, h->cepoch, 0u, 1u, h->stream));
+            h->st.gpu_launches += 1;
             CK(h, launch_even_inc(h->G, h->stream));
             h->st.gpu_launches += 4;
         } else {
@@ -654,10 +674,9 @@ pg_status even_switch(pg_game h, int64_t *count) {
         if (inc) h->st.inc_even_switches++;
     }
     // a new C starts: changes after this All_Even
-    h->G.cepoch = ++h->cepoch;
-    if (h->G.cepoch == 0) {
+    if (++h->cepoch == 0) {
         CK(h, cudaMemsetAsync(h->G.cmark, 0, sizeof(uint32_t) * ((size_t)h->G.n_int + 1), h->stream));
-        h->G.cepoch = ++h->cepoch;
+        ++h->cepoch;
     }
     CK(h, cudaMemsetAsync(&h->G.ctl->nC, 0, sizeof(unsigned long long), h->stream));
     h->h_ctl->nC = 0;
@@ -725,6 +744,107 @@ pg_status outputs_end(pg_game h, std::vector<OutBuf> &outs) {
     return PG_OK;
 }
 
+// Algorithm 1 as one graph launch (pg_loop.cu): the inner and outer loops, the
+// incremental / from-scratch decisions and the counts all run on the device; the host
+// waits once, then reads the loop's status. Host fixes (splitter buffers, wrapped
+// epoch marks) relaunch the graph, which resumes from the state kept in Ctl.
+pg_status solve_graph(pg_game h, int64_t *inner, int64_t *outer) {
+    DevGame &G = h->G;
+    if (!h->cap_stream) CK(h, cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
+    auto ensure_graph = [&]() -> pg_status {
+        if (h->loop_exec) return PG_OK;
+        LoopCfg c{};
+        c.n_int = G.n_int;
+        c.n_even = G.n_even;
+        c.max_inner = h->max_inner;
+        c.max_outer = h->max_outer;
+        c.s_div = h->inc_s_div;
+        c.s_div_even = h->inc_s_div_even;
+        c.inc_ok = G.dp <= 32 && !(h->flags & PG_NO_INCREMENTAL);
+        c.si_reset = (h->flags & PG_SI_RESET) != 0;
+        c.inc_max_steps = (int32_t)std::min<int64_t>(h->inc_max_steps, 1 << 20);
+        c.inc_grid_mul = std::max(1, G.inc_grid_mul);
+        const int cap = std::max(1, h->lc.coop_inc);
+        c.grid_class[0] = 1;
+        c.grid_class[1] = std::min(cap, 8);
+        c.grid_class[2] = std::min(cap, 64);
+        c.grid_class[3] = cap;
+        c.K = G.K;
+        const cudaError_t e = build_loop_graph(G, h->lc, c, h->cap_stream, &h->loop_exec, &h->loop_nodes);
+        if (e != cudaSuccess) {
+            set_err(std::string("build_loop_graph (pg_loop.cu:") + std::to_string(g_loop_graph_fail_line) +
+                    "): " + cudaGetErrorString(e));
+            h->broken = true;
+            return PG_ECUDA;
+        }
+        return PG_OK;
+    };
+    pg_status rc = PG_OK;
+    if ((rc = ensure_graph())) return rc;
+    CK(h, launch_loop_init(G.ctl, h->epoch, h->cepoch, h->stream));
+    for (int relaunch = 0;; relaunch++) {
+        if ((rc = ensure_graph())) return rc;
+        CK(h, cudaGraphLaunch(h->loop_exec, h->stream));
+        if ((rc = readback(h))) return rc;
+        const Ctl &c = *h->h_ctl;
+        if (c.ls_status == LS_HOST_SPLITTERS) {          // grow, rebuild (pointers are baked in), resume
+            if ((rc = grow_splitters(h, (int64_t)c.nspl))) return rc;
+            cudaGraphExecDestroy(h->loop_exec);
+            h->loop_exec = nullptr;
+            CK(h, cudaMemsetAsync(&G.ctl->ls_status, 0, sizeof(unsigned long long), h->stream));
+            continue;
+        }
+        if (c.ls_status == LS_HOST_EPOCHS) {             // clear the wrapped marks, resume
+            const size_t N1 = (size_t)G.n_int + 1;
+            CK(h, cudaMemsetAsync(G.dmark, 0, sizeof(uint32_t) * N1, h->stream));
+            CK(h, cudaMemsetAsync(G.emark, 0, sizeof(uint32_t) * N1, h->stream));
+            CK(h, cudaMemsetAsync(G.cmark, 0, sizeof(uint32_t) * N1, h->stream));
+            CK(h, launch_loop_epochs_cleared(G.ctl, h->stream));
+            continue;
+        }
+        break;
+    }
+    const Ctl &c = *h->h_ctl;
+    *inner = c.ls_inner;
+    *outer = c.ls_outer;
+    h->epoch = c.ls_epoch;
+    h->cepoch = c.ls_cepoch;
+    h->have_state = false;
+    h->c_valid = false;
+    const unsigned long long *st = c.ls_st;
+    const double np_ = (double)G.n_int;
+    const int64_t F = (int64_t)st[LST_FULL_VALS], I = (int64_t)st[LST_INC_LAUNCHES];
+    h->st.odd_switches += (int64_t)st[LST_ODD_SW];
+    h->st.even_switches += (int64_t)st[LST_EVEN_SW];
+    h->st.inc_valuations += (int64_t)st[LST_INC_STEPS];
+    h->st.inc_aborts += (int64_t)st[LST_INC_ABORTS];
+    h->st.inc_even_switches += (int64_t)st[LST_EVEN_INC];
+    h->st.dirty_vertices += (int64_t)st[LST_DIRTY];
+    h->st.walk_steps += (int64_t)st[LST_WALK];
+    h->st.v1_rounds += (int64_t)st[LST_V1_ROUNDS];
+    h->st.full_compares += (int64_t)st[LST_FULL_CMP];
+    h->st.prefix_gathers += (int64_t)st[LST_CPX];
+    h->st.top_vertices += (int64_t)st[LST_TOP];
+    h->st.v2_split_valuations += (int64_t)st[LST_SPLIT_VALS];
+    h->st.max_depth = std::max<int64_t>(h->st.max_depth, (int64_t)st[LST_MAXDEPTH]);
+    h->st.bytes_v1 += 5.0 * np_ * (double)F;
+    h->st.bytes_v2 += 41.0 * np_ * (double)F;
+    // work kernels (V1 + 4 splitter + V2 + 3 switch per full valuation; 1 per
+    // incremental launch; 4 / 3 per All_Even over C / over all) and control kernels
+    h->st.gpu_launches += 9 * F + I + 4 * (int64_t)st[LST_EVEN_INC] + 3 * (int64_t)st[LST_EVEN_FULL] +
+                          2 * (F + I) + 3 * *outer + 1;
+    h->st.device_loop_solves++;
+    if (c.ls_status == LS_CAP_INNER || c.ls_status == LS_CAP_OUTER) {
+        set_err(c.ls_status == LS_CAP_OUTER ? "outer pass cap reached" : "inner iteration cap reached");
+        return PG_EITERCAP;
+    }
+    if (c.ls_status != LS_DONE) {
+        set_err("device loop ended in state " + std::to_string(c.ls_status));
+        return PG_ECUDA;
+    }
+    return PG_OK;
+}
+
 double now_ms() {
     using namespace std::chrono;
     return duration<double, std::milli>(steady_clock::now().time_since_epoch()).count();
@@ -752,6 +872,8 @@ void pg_free(pg_game h) try {
         else cudaFree(p);
     }
     if (h->stream) cudaStreamSynchronize(h->stream);
+    if (h->loop_exec) cudaGraphExecDestroy(h->loop_exec);
+    if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
     if (h->h_ctl) cudaFreeHost(h->h_ctl);
     if (h->h_x) cudaFreeHost(h->h_x);
     for (auto e : h->ev_pool) cudaEventDestroy(e);
@@ -774,7 +896,9 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     h->flags = o.flags;
     h->max_inner = o.max_inner;
     h->trace = getenv("PGSI_TRACE") && (getenv("PGSI_TRACE")[0] == '1' || getenv("PGSI_TRACE")[0] == '2');
-    h->G.trace_ts = getenv("PGSI_TRACE") && getenv("PGSI_TRACE")[0] == '2';
+    h->G.trace_ts = getenv("PGSI_TRACE") && (getenv("PGSI_TRACE")[0] == '2' || getenv("PGSI_TRACE")[0] == '3');
+    const bool trace_levels = getenv("PGSI_TRACE") && getenv("PGSI_TRACE")[0] == '3';
+    h->trace = h->trace || trace_levels;
     h->max_outer = o.max_outer;
     DeviceGuard dg(h->device);
     auto fail = [&](pg_status r) { pg_free(h); return r; };
@@ -914,9 +1038,12 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     CKL(cudaMemsetAsync(G.dmark, 0, sizeof(uint32_t) * N1, s));
     CKL(cudaMemsetAsync(G.emark, 0, sizeof(uint32_t) * N1, s));
     CKL(cudaMemsetAsync(G.cmark, 0, sizeof(uint32_t) * N1, s));
-    G.epoch = 0;
-    G.cepoch = 1;
+    h->epoch = 0;
     h->cepoch = 1;
+    if (getenv("PGSI_EPOCH_START")) {   // testing: start the mark epochs near the 2^32 wrap
+        h->epoch = (uint32_t)strtoul(getenv("PGSI_EPOCH_START"), nullptr, 0);
+        h->cepoch = std::max<uint32_t>(1u, h->epoch);
+    }
     // incremental-step thresholds (tuning knobs; results never depend on them)
     G.inc_max_levels = getenv("PGSI_INC_MAX_LEVELS") ? atoi(getenv("PGSI_INC_MAX_LEVELS")) : 256;
     G.bfs_max_levels = getenv("PGSI_BFS_MAX_LEVELS") ? atoi(getenv("PGSI_BFS_MAX_LEVELS")) : 160;
@@ -928,13 +1055,18 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     G.inc_grid_cap = h->lc.coop_inc;
     G.inc_grid_mul = getenv("PGSI_INC_GRID_MUL") ? atoi(getenv("PGSI_INC_GRID_MUL")) : 16;
     if (getenv("PGSI_SMALL_MAX")) h->small_max = atoll(getenv("PGSI_SMALL_MAX"));
+    if (getenv("PGSI_DEVICE_LOOP")) h->device_loop = atoi(getenv("PGSI_DEVICE_LOOP")) != 0;
     if (cudaDeviceGetAttribute(&h->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device) != cudaSuccess)
         h->smem_optin = 48 * 1024;
     G.inc_e_in_v2 = getenv("PGSI_INC_E_V2") ? atoi(getenv("PGSI_INC_E_V2")) : 1;
     G.inc_fuse_e = getenv("PGSI_INC_FUSE_E") ? atoi(getenv("PGSI_INC_FUSE_E")) : 0;   // measured slower
     G.inc_skip_v1 = getenv("PGSI_INC_SKIP_V1") ? atoi(getenv("PGSI_INC_SKIP_V1")) : 1;
     G.inc_blk_frontier = getenv("PGSI_INC_BLK") ? atoi(getenv("PGSI_INC_BLK")) : 256;
-    G.inc_max_steps = 1;
+    G.lvlog = nullptr;
+    if (trace_levels) {
+        CKL(dalloc(h, &G.lvlog, 8192));
+        CKL(cudaMemsetAsync(G.lvlog, 0, 8, s));
+    }
     // children CSR scratch of the BFS valuation (§V-bfs)
     CKL(dalloc(h, &G.ccnt, N1));
     CKL(dalloc(h, &G.cptr, N1));
@@ -1164,7 +1296,16 @@ pg_status pg_solve(pg_game h, uint8_t *winner, int32_t *sigma, int32_t *tau, int
                 rc = PG_EINADMISSIBLE;
             }
         }
-        for (; !small;) {                                    // Algorithm 1, outer repeat
+        // Algorithm 1 on the device (pg_loop.cu) unless a host-side feature is on:
+        // per-phase CUDA events, the trace, sharding, the BFS valuation, the
+        // Bellman-Ford arm, or odd-cycle checks (cycle-dominant priorities)
+        const bool graph = !small && h->device_loop && !check && !h->dist_fn && !h->trace &&
+                           !(h->flags & (PG_PHASE_TIMING | PG_TRACE | PG_BFS | PG_BELLMAN_FORD));
+        if (graph) {
+            PhaseScope ps(h, PH_OTHER);
+            rc = solve_graph(h, &inner, &outer);
+        }
+        for (; !small && !graph;) {                          // Algorithm 1, outer repeat
             if (h->max_outer > 0 && outer >= h->max_outer) {
                 set_err("outer pass cap reached");
                 rc = PG_EITERCAP;

@@ -78,6 +78,27 @@ struct Ctl {
     unsigned int bar_count;         // grid barrier
     unsigned int bar_gen;
     unsigned long long ts[12];      // PGSI_TRACE=2: %globaltimer at the incremental kernel's phase ends
+    // ---- launch parameters of k_inc_iter / k_ebuild_even, read from device memory so
+    // that the same kernels run from the host loop and from the device-resident one
+    // (pg_loop.cu): written by k_set_launch_params or by the loop's control kernels
+    unsigned int lp_epoch;          // D / E mark epoch of the launch's first step
+    unsigned int lp_cepoch;         // epoch of C (changes since the last All_Even)
+    unsigned int lp_s_odd;          // the first step's switch list came from All_Odd
+    unsigned int lp_max_steps;      // inner iterations the launch may run
+    // ---- device-resident Algorithm 1 (pg_loop.cu) ----
+    long long ls_inner, ls_outer;   // valuations computed, outer passes (readings 11-12)
+    unsigned long long ls_status;   // LS_RUNNING / LS_DONE / LS_CAP_INNER / LS_CAP_OUTER / LS_HOST_*
+    unsigned long long ls_last_nsw; // |S| of the last switch step
+    unsigned int ls_have_state;     // jl / cpx / top describe the profile before the last switches
+    unsigned int ls_last_sw_odd;    // ... which came from All_Odd
+    unsigned int ls_c_valid;        // C covers every change since the last All_Even
+    unsigned int ls_force_full;     // the last incremental launch aborted: next valuation from scratch
+    unsigned int ls_mode;           // body the last SWITCH ran (LM_*)
+    unsigned int ls_even_inc;       // the last All_Even ran over C
+    unsigned int ls_epoch;          // last reserved D / E epoch
+    unsigned int ls_cepoch;         // current C epoch
+    unsigned int ls_resume;         // relaunch after a host fix: 1 = inside the inner loop, 2 = at All_Even
+    unsigned long long ls_st[24];   // statistics accumulators (LST_*)
 };
 #define PGSI_CTL_RESET_BYTES offsetof(pgsi::Ctl, bad_index)
 
@@ -108,10 +129,8 @@ struct DevGame {
     int32_t *Dl;        // D list
     uint2 *Dr;          // reverse-CSR range [rrp[v], rrp[v+1]) of each D-list entry
     int32_t *El;        // E list
-    uint32_t epoch;     // current incremental epoch
     uint32_t *cmark;    // epoch marks: v in C
     int32_t *Cl;        // C list
-    uint32_t cepoch;    // epoch of C (one per outer pass)
     int32_t inc_max_levels;   // abort the incremental step beyond this closure depth
     int64_t inc_max_dirty;    // ... or this closure size
     int32_t bfs_max_levels;   // full valuation by top-down BFS up to this depth
@@ -136,11 +155,10 @@ struct DevGame {
     int64_t sh_even_lo, sh_even_hi, sh_odd_lo, sh_odd_hi;
     int32_t sharded;
     int32_t trace_ts;   // PGSI_TRACE=2: record phase timestamps in ctl->ts
-    int32_t inc_max_steps;  // inner iterations one k_inc_iter launch may run (>= 1)
+    unsigned long long *lvlog;   // PGSI_TRACE=3: closure level log (else null)
     int32_t inc_grid_cap;   // cooperative grid cap of k_inc_iter
     int32_t inc_grid_mul;   // k_inc_iter grid = |S| * inc_grid_mul threads (capped)
     int64_t inc_s_div;      // incremental step only while |S| * inc_s_div <= n'
-    int32_t inc_s_odd;      // the switch list S of the first incremental step came from All_Odd
     int32_t inc_fuse_e;     // build E inside the dirty-closure scan (else a separate pass)
     int32_t inc_e_in_v2;    // build E in the V2-on-D pass (else a separate pass)
     int32_t inc_skip_v1;    // after All_Odd steps replace V1 on D by the V2 walk depth
@@ -155,6 +173,38 @@ struct LaunchCfg {
     int coop_inc = 0;
     int coop_bfs = 0;
 };
+
+// device-resident Algorithm 1 (pg_loop.cu): loop status and statistics slots
+enum { LS_RUNNING = 0, LS_DONE = 1, LS_CAP_INNER = 2, LS_CAP_OUTER = 3, LS_HOST_SPLITTERS = 4, LS_HOST_EPOCHS = 5 };
+enum { LM_INC0 = 0, LM_INC1, LM_INC2, LM_INC3, LM_FULL = 4, LM_NONE = 5 };   // SWITCH bodies of the inner loop
+enum {
+    LST_FULL_VALS = 0, LST_INC_LAUNCHES, LST_INC_STEPS, LST_INC_ABORTS, LST_ODD_SW, LST_EVEN_SW,
+    LST_EVEN_INC, LST_EVEN_FULL, LST_DIRTY, LST_NE_SUM, LST_WALK, LST_V1_ROUNDS, LST_MAXDEPTH,
+    LST_ROWS_ODD, LST_CPX, LST_FULL_CMP, LST_TOP, LST_SPLIT_VALS, LST_ROWS_EVEN, LST_NE_EVEN,
+    LST_NC, LST_ODD_SW_FULL, LST_N
+};
+static_assert(LST_N <= 24, "ls_st");
+
+// configuration of the device-resident loop (constant for a solve)
+struct LoopCfg {
+    int64_t n_int, n_even;
+    int64_t max_inner, max_outer;   // caps (0 = none)
+    int64_t s_div, s_div_even;      // incremental step when |S| * s_div <= n' (S from All_Odd / All_Even)
+    int32_t inc_ok;                 // incremental valuation allowed (dp <= 32, no PG_NO_INCREMENTAL)
+    int32_t si_reset;               // PG_SI_RESET
+    int32_t inc_max_steps;          // inner iterations per incremental launch
+    int32_t inc_grid_mul;           // k_inc_iter grid = |S| * mul threads
+    int32_t grid_class[4];          // k_inc_iter grid sizes of the SWITCH bodies LM_INC0..3
+    int32_t K;                      // splitter stride (statistics)
+};
+cudaError_t launch_set_launch_params(Ctl *ctl, uint32_t epoch, uint32_t cepoch, uint32_t s_odd, uint32_t max_steps,
+                                     cudaStream_t s);
+cudaError_t launch_loop_init(Ctl *ctl, uint32_t epoch, uint32_t cepoch, cudaStream_t s);
+cudaError_t launch_loop_epochs_cleared(Ctl *ctl, cudaStream_t s);
+// builds and instantiates the graph of Algorithm 1 (pg_loop.cu); cs = a capture stream
+extern int g_loop_graph_fail_line;
+cudaError_t build_loop_graph(const DevGame &g, const LaunchCfg &lc, const LoopCfg &c, cudaStream_t cs,
+                             cudaGraphExec_t *exec, int *nodes);
 
 // kernels (pg_kernels.cu); every launcher returns the cudaError_t of the launch
 cudaError_t launch_init_profile(const DevGame &g, cudaStream_t s);

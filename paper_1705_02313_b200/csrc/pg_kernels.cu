@@ -1187,6 +1187,19 @@ __device__ __forceinline__ void expand_closure(const DevGame &g, int32_t f, uint
     }
 }
 
+// PGSI_TRACE=3: one (frontier width | level << 32 | block mode << 63, %globaltimer)
+// record per closure level (debugging the closure's level structure)
+__device__ __forceinline__ void trace_level(const DevGame &g, int64_t width, int level, bool blk) {
+    if (!g.lvlog) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const unsigned long long k = atomicAdd(g.lvlog, 1ull);
+    if (k < 4095) {
+        g.lvlog[2 + 2 * k] = (unsigned long long)width | ((unsigned long long)level << 32) | (blk ? (1ull << 63) : 0ull);
+        g.lvlog[3 + 2 * k] = t;
+    }
+}
+
 __device__ __forceinline__ void trace_ts(const DevGame &g, int k) {
     if (g.trace_ts && blockIdx.x == 0 && threadIdx.x == 0) {
         unsigned long long t;
@@ -1208,9 +1221,11 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
 
     // Consecutive inner iterations run in this one launch (Algorithm 1's inner
     // loop, kept on the device) while each stays incremental;
-    // step t uses epoch g.epoch + t for its D / E marks (the host reserves them).
+    // step t uses epoch lp_epoch + t for its D / E marks (reserved by the caller).
+    const uint32_t epoch0 = __ldcg(&ctl->lp_epoch), cepoch = __ldcg(&ctl->lp_cepoch);
+    const uint32_t s_odd = __ldcg(&ctl->lp_s_odd), max_steps = __ldcg(&ctl->lp_max_steps);
     for (int step = 0;; step++) {
-    const uint32_t ep = g.epoch + (uint32_t)step;
+    const uint32_t ep = epoch0 + (uint32_t)step;
     if (blockIdx.x == 0 && threadIdx.x == 0) ctl->steps_done = (unsigned long long)step;
     trace_ts(g, 0);
     // ---- 1. dirty closure
@@ -1263,6 +1278,7 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
                     __syncthreads();
                     blo = bhi;
                     bhi += (int64_t)*bc;
+                    if (threadIdx.x == 0) trace_level(g, bhi - blo, blev, true);
                     if (blev >= g.inc_max_levels || bhi > g.inc_max_dirty) { abort = true; break; }
                 }
                 if (threadIdx.x == 0) {
@@ -1299,6 +1315,7 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
         if (blockIdx.x == 0 && threadIdx.x == 0) ctl->dcnt[(glev + 2) % 3] = 0;
         lo = hi;
         hi += added;
+        if (blockIdx.x == 0 && threadIdx.x == 0) trace_level(g, added, levels, false);
         if (levels >= g.inc_max_levels || hi > g.inc_max_dirty) {
             // deep or huge closure: a from-scratch valuation is cheaper. Nothing but
             // marks (epoch-scoped) has been written; the host redoes the step in full.
@@ -1317,7 +1334,7 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
     // walk: depth(v) = walk length + depth(x) at the first clean vertex x. (A walk
     // ending at a clean ⊤ vertex would contradict this; it sets inc_overflow and the
     // host redoes the step in full, so results never depend on the argument.)
-    const bool odd_s = (step > 0 || g.inc_s_odd) && g.inc_skip_v1;
+    const bool odd_s = (step > 0 || s_odd) && g.inc_skip_v1;
     unsigned long long *jl = g.jl;
     int r = 0;
     if (!odd_s) {
@@ -1331,8 +1348,8 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
             v = __ldcg(g.Dl + i);
             jl[v] = pack_jl((uint32_t)__ldcg(g.succ + v), 1u);
         }
-        const bool addc = v >= 0 && __ldcg(g.cmark + v) != g.cepoch;
-        if (addc) g.cmark[v] = g.cepoch;
+        const bool addc = v >= 0 && __ldcg(g.cmark + v) != cepoch;
+        if (addc) g.cmark[v] = cepoch;
         warp_append(addc, v, g.Cl, &ctl->nC);
     }
     gbar(ctl);
@@ -1387,8 +1404,8 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
         uint2 rr = make_uint2(0u, 0u);
         if (e_in_v2 && v >= 0) rr = __ldcg(g.Dr + i);
         if (odd_s) {
-            const bool addc = v >= 0 && __ldcg(g.cmark + v) != g.cepoch;
-            if (addc) g.cmark[v] = g.cepoch;
+            const bool addc = v >= 0 && __ldcg(g.cmark + v) != cepoch;
+            if (addc) g.cmark[v] = cepoch;
             warp_append(addc, v, g.Cl, &ctl->nC);
         }
         if (v >= 0) {
@@ -1514,7 +1531,7 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
         ctl->nE = 0;
     }
     const int64_t need = (nsn * g.inc_grid_mul + kThreads - 1) / kThreads;   // the grid the host would pick
-    if (sw == 0 || step + 1 >= g.inc_max_steps || nsn * g.inc_s_div > N ||
+    if (sw == 0 || step + 1 >= (int)max_steps || nsn * g.inc_s_div > N ||
         (need > (int64_t)gridDim.x && (int)gridDim.x < g.inc_grid_cap))
         return;
     gbar(ctl);   // the resets above precede the next step's appends
@@ -1526,7 +1543,7 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
 // of the dirty sets since the previous All_Even); no other Even decision can
 // change (its candidates' val^σ are unchanged since it was last evaluated).
 __global__ void __launch_bounds__(kThreads) k_ebuild_even(DevGame g) {
-    const uint32_t ep = g.epoch;
+    const uint32_t ep = __ldcg(&g.ctl->lp_epoch);
     const int lane = threadIdx.x & 31;
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -1948,6 +1965,19 @@ cudaError_t launch_inc_iter(const DevGame &g, const LaunchCfg &lc, cudaStream_t 
     DevGame gg = g;
     void *args[] = {&gg};
     return cudaLaunchCooperativeKernel((const void *)k_inc_iter, dim3((unsigned)grid), dim3(kThreads), args, 0, s);
+}
+
+__global__ void k_set_launch_params(Ctl *ctl, uint32_t epoch, uint32_t cepoch, uint32_t s_odd, uint32_t max_steps) {
+    ctl->lp_epoch = epoch;
+    ctl->lp_cepoch = cepoch;
+    ctl->lp_s_odd = s_odd;
+    ctl->lp_max_steps = max_steps;
+}
+
+cudaError_t launch_set_launch_params(Ctl *ctl, uint32_t epoch, uint32_t cepoch, uint32_t s_odd, uint32_t max_steps,
+                                     cudaStream_t s) {
+    k_set_launch_params<<<1, 1, 0, s>>>(ctl, epoch, cepoch, s_odd, max_steps);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_export_val(const DevGame &g, int64_t count, int32_t *val_out, uint8_t *top_out,
