@@ -8,8 +8,11 @@ PAPER.md:548-561: every valuation and every All_Odd / All_Even switch until no
 switch remains) of that game, inputs resident in HBM (pg_load done before the
 timed region). Timing: CUDA events on the library's stream (torch's current
 stream), W untimed warm-up steps, K timed steps bracketed by barrier +
-synchronize, max over ranks. N > 1 GPUs: one independent game per rank
-(weak scaling, no data-path collective).
+synchronize, max over ranks. N > 1 GPUs (torchrun): by default ONE game sharded
+over the ranks (strong scaling; the switch steps split by vertex range, switch lists
+all-gathered by NCCL inside libpgsi, pg_dist_init; outputs checked byte-identical to a
+one-GPU solve in the same run); ``--mode replicas``: an independent game per rank
+(weak scaling, no data-path collective). DESIGN.md "Multi-GPU".
 
 Extra keys: ``e2e`` = the same metric through the public API from pinned host
 buffers (pg_load incl. host transform + H2D, pg_solve, D2H of winner/σ/τ each
@@ -237,6 +240,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-arms", action="store_true", help="skip the SI-Reset / Bellman-Ford arms")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e/cpu/clocks)")
+    ap.add_argument("--mode", default="sharded", choices=["sharded", "replicas"],
+                    help="N > 1: one game sharded over the ranks (strong scaling, pg_dist_init / NCCL; "
+                         "default) or an independent game per rank (weak scaling)")
+    ap.add_argument("--force-shard", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     wl = WORKLOADS[args.workload]
 
@@ -257,10 +264,20 @@ def main():
 
     dev = torch.device("cuda", local)
     stream = torch.cuda.current_stream(dev)
-    game = make_game(wl, pgdist.game_seed(args.seed, rank))   # weak scaling: an independent game per rank
+    # --force-shard: the sharded path even on one GPU (NCCL world = 1; exercises it)
+    sharded = (world > 1 and args.mode == "sharded") or args.force_shard
+    # sharded: every rank loads the same game; replicas: an independent game per rank
+    game = make_game(wl, args.seed if sharded else pgdist.game_seed(args.seed, rank))
     # timed solves: the default path (Algorithm 1 as one CUDA graph launch per solve for
-    # large games, pg_loop.cu; one single-block kernel for small ones)
+    # large games, pg_loop.cu; one single-block kernel for small ones; the host-driven
+    # loop with a switch-list exchange per step when sharded)
     G = Game.from_game(game, device=local, stream=stream.cuda_stream, device_ptrs=True)
+    nccl_id = pgdist.nccl_join(G, dist, rank, world) if sharded else None
+
+    def join(h):   # another handle of the same sharded solve: the same communicator
+        if sharded:
+            h.dist_init(nccl_id, rank, world)
+        return h
     n = game.n
     out = (torch.empty(n, dtype=torch.uint8, device=dev), torch.empty(n, dtype=torch.int32, device=dev),
            torch.empty(n, dtype=torch.int32, device=dev), None)
@@ -293,8 +310,24 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize(dev)
     barrier()
-    ms, units = pgdist.reduce_time_and_units(dist, e0.elapsed_time(e1), float(n) * acc["inner_iters"], dev)
+    if sharded:   # one game: its valuations once, over the slowest rank's time
+        ms = pgdist.reduce_max(dist, e0.elapsed_time(e1), dev)
+        units = float(n) * acc["inner_iters"]
+    else:
+        ms, units = pgdist.reduce_time_and_units(dist, e0.elapsed_time(e1), float(n) * acc["inner_iters"], dev)
     value = units / (ms / 1000.0)
+    # sharded: the outputs must be byte-identical to one GPU's (rank 0 re-solves alone)
+    identical = None
+    if sharded:
+        got = [t.cpu().numpy() for t in out[:3]]
+        if rank == 0:
+            G1 = Game.from_game(game, device=local, stream=stream.cuda_stream)
+            r1 = G1.solve()
+            identical = bool(np.array_equal(got[0], r1.winner) and np.array_equal(got[1], r1.sigma) and
+                             np.array_equal(got[2], r1.tau) and r1.stats["inner_iters"] * args.steps ==
+                             acc["inner_iters"])
+            G1.free()
+        barrier()
     inner = int(acc["inner_iters"] / args.steps)
     outer = int(acc["outer_passes"] / args.steps)
     timed_stats = dict(acc)
@@ -302,7 +335,7 @@ def main():
     # ---- per-phase CUDA events (PG_PHASE_TIMING): kernel times for the roofline block.
     # Events around every phase need the host-driven loop, so these are separate solves of
     # the same game right after the timed region (same kernels, same launch sequence).
-    Gp = Game.from_game(game, device=local, stream=stream.cuda_stream, device_ptrs=True, phase_timing=True)
+    Gp = join(Game.from_game(game, device=local, stream=stream.cuda_stream, device_ptrs=True, phase_timing=True))
     Gp.solve(out=out)
     acc = {k: 0.0 for k in acc}
     torch.cuda.synchronize(dev)
@@ -347,8 +380,8 @@ def main():
     # ---- the same solve with every valuation recomputed from scratch (no §V-inc)
     scratch = None
     if not args.profile:
-        Gs = Game.from_game(game, device=local, stream=stream.cuda_stream, device_ptrs=True,
-                            incremental=False)
+        Gs = join(Game.from_game(game, device=local, stream=stream.cuda_stream, device_ptrs=True,
+                                 incremental=False))
         for _ in range(2):
             Gs.solve(out=out)
         barrier()
@@ -360,7 +393,10 @@ def main():
             s_units += float(n) * rs.stats["inner_iters"]
         e1.record(stream)
         torch.cuda.synchronize(dev)
-        sms, s_units = pgdist.reduce_time_and_units(dist, e0.elapsed_time(e1), s_units, dev)
+        if sharded:
+            sms = pgdist.reduce_max(dist, e0.elapsed_time(e1), dev)
+        else:
+            sms, s_units = pgdist.reduce_time_and_units(dist, e0.elapsed_time(e1), s_units, dev)
         scratch = {"value": s_units / (sms / 1000.0), "ms_per_step": sms / args.steps,
                    "note": "PG_NO_INCREMENTAL: every valuation recomputed for all vertices"}
         Gs.free()
@@ -376,8 +412,8 @@ def main():
             # Bellman-Ford needs as many rounds as the longest shortest path (4M on F_deep):
             # capped so that the bench stays bounded; a capped arm is reported as such
             cap = 20000 if arm == "bf" else 0
-            Ga = Game.from_game(game, device=local, stream=stream.cuda_stream, device_ptrs=True,
-                                phase_timing=True, best_response=arm, max_inner=cap)
+            Ga = join(Game.from_game(game, device=local, stream=stream.cuda_stream, device_ptrs=True,
+                                     phase_timing=True, best_response=arm, max_inner=cap))
             try:
                 Ga.solve(out=out)
             except PGError as exc:
@@ -431,7 +467,7 @@ def main():
         e0.record(stream)
         e_units = 0.0
         for _ in range(e2e_steps):
-            Ge = Game(n, rp, col, own, pri, device=local, stream=stream.cuda_stream)
+            Ge = join(Game(n, rp, col, own, pri, device=local, stream=stream.cuda_stream))
             re = Ge.solve(out=(hw, hs, ht, None))
             e_units += float(n) * re.stats["inner_iters"]
             Ge.free()
@@ -439,7 +475,10 @@ def main():
         torch.cuda.synchronize(dev)
         ems = e0.elapsed_time(e1)
         wall_ms = 1000 * (time.perf_counter() - t0)
-        ems, e_units = pgdist.reduce_time_and_units(dist, max(ems, wall_ms), e_units, dev)
+        if sharded:
+            ems = pgdist.reduce_max(dist, max(ems, wall_ms), dev)
+        else:
+            ems, e_units = pgdist.reduce_time_and_units(dist, max(ems, wall_ms), e_units, dev)
         e2e = {"value": e_units / (ems / 1000.0), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": ems / e2e_steps, "steps": e2e_steps,
                "includes": "pg_load (H2D of the raw CSR, then validate / canonicalise / preprocess / reorder on the GPU) + pg_solve + D2H of winner, sigma, tau"}
@@ -459,7 +498,8 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic",
             "config": {"workload": wl["desc"], "n": n, "d": G.d, "out_degree": f"{wl.get('lo', '-')}-{wl.get('hi', '-')}",
                        "seed": args.seed, "n_internal": G.n_internal, "m": int(game.m),
                        "inner_iters": inner, "outer_passes": outer, "solve_ms": ms / args.steps,
@@ -473,7 +513,11 @@ def main():
                                 if timed_stats["device_loop_solves"] else
                                 "single-block whole-solve kernel" if timed_stats["small_solves"] else "host-driven"),
                        "host_loop_ms_per_solve": host_loop_ms,
-                       "parallelism": "single GPU" if world == 1 else f"weak: {world} independent games",
+                       "parallelism": ("single GPU" if world == 1 else
+                                       f"strong: one game, switch steps sharded over {world} GPUs, valuation "
+                                       f"replicated, switch lists all-gathered by NCCL inside libpgsi "
+                                       f"(SURVEY §8(e) M2)" if sharded else f"weak: {world} independent games"),
+                       "sharded_identical_to_1gpu": identical,
                        "l2": f"inputs larger than L2: per-iteration working set {ws_bytes / 1e9:.2f} GB "
                              f"(prefixes, jl, succ, pidx, ⊤, CSR) > 126 MB; no flush needed"},
             "roofline": roofline,

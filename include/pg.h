@@ -285,6 +285,28 @@ typedef int (*pg_allgather_fn)(void *ctx, const void *send, void *recv, int64_t 
 pg_status pg_dist_attach(pg_game g, int32_t rank, int32_t world, pg_allgather_fn fn,
                          void *ctx);
 
+/* Multi-GPU with the library's own NCCL communicator (SURVEY.md §8(b) pg_dist_init;
+ * §8(e) M2): the same sharding as pg_dist_attach, with the per-step switch-list
+ * exchange done by ncclAllGather on the handle's stream (sizes gathered device to
+ * device, then the lists, padded to the largest) — no caller callback.
+ *
+ * pg_dist_unique_id: a fresh ncclUniqueId (rank 0 creates it and sends it to the
+ * other ranks out of band, e.g. torch.distributed.broadcast_object_list).
+ *   id, bytes     caller buffer of at least 128 bytes (sizeof(ncclUniqueId))
+ * Errors: PG_EINVAL (buffer too small), PG_ENCCL. */
+pg_status pg_dist_unique_id(void *id, int64_t bytes);
+
+/* pg_dist_init: make the handle rank `rank` of `world` ranks solving the SAME game
+ * (identical pg_load inputs and flags on every rank, one GPU per rank, collective
+ * calls in the same order), each evaluating All_Odd / All_Even on its contiguous
+ * shard of the Odd and of the Even vertex range (switchability is local to a vertex,
+ * PAPER.md:575-582). Results (winners, strategies, valuations, counts) are identical
+ * to world = 1. world = 1 is allowed and runs the exchange through NCCL too.
+ * Replaces a pg_dist_attach callback; pg_dist_attach(g, 0, 1, NULL, NULL) detaches.
+ *   id            the ncclUniqueId bytes from pg_dist_unique_id on rank 0
+ * Errors: PG_EINVAL, PG_ENCCL (ncclCommInitRank or a later collective failed). */
+pg_status pg_dist_init(pg_game g, const void *id, int32_t rank, int32_t world);
+
 /* ---- PGSolver interchange and solution verification (host-side
  * native code, no GPU, no handle) ------------------------------------------------ */
 

@@ -17,6 +17,19 @@ def nvcc():
     return "nvcc"
 
 
+def nccl_dirs():
+    """(include, lib) of the NCCL that torch loads (nvidia-nccl wheel), else the system's."""
+    try:
+        import nvidia.nccl as nn
+        base = list(nn.__path__)[0]
+        inc, lib = os.path.join(base, "include"), os.path.join(base, "lib")
+        if os.path.exists(os.path.join(inc, "nccl.h")):
+            return inc, lib
+    except ImportError:
+        pass
+    return "/usr/include", "/usr/lib/x86_64-linux-gnu"
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
     deps = srcs + [os.path.join(CSRC, "pg_internal.cuh"), os.path.join(ROOT, "include", "pg.h")]
@@ -24,9 +37,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
         t = os.path.getmtime(LIB)
         if all(os.path.getmtime(d) <= t for d in deps):
             return LIB
+    ninc, nlib = nccl_dirs()
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-           "-Xptxas", "-v" if verbose else "-O3", "-I", os.path.join(ROOT, "include"),
-           "-o", LIB + ".tmp", *srcs]
+           "-Xptxas", "-v" if verbose else "-O3", "-I", os.path.join(ROOT, "include"), "-I", ninc,
+           "-o", LIB + ".tmp", *srcs, "-L", nlib, "-l:libnccl.so.2", "-Xlinker", f"-rpath={nlib}"]
     subprocess.check_call(cmd)
     os.replace(LIB + ".tmp", LIB)
     return LIB

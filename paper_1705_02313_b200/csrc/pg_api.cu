@@ -9,7 +9,11 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <map>
+#include <mutex>
 #include <vector>
+
+#include <nccl.h>
 
 #include "pg_internal.cuh"
 #include "pg_guard.h"
@@ -65,6 +69,8 @@ struct pg_game_s {
     uint32_t cepoch = 0;
     // multi-GPU switch sharding (pg_dist_attach)
     pg_allgather_fn dist_fn = nullptr;
+    ncclComm_t nccl = nullptr;        // pg_dist_init: the library's own NCCL communicator
+    unsigned long long *d_cnts = nullptr;   // world switch-list sizes (NCCL all-gather target)
     void *dist_ctx = nullptr;
     int32_t dist_rank = 0, dist_world = 1;
     int2 *swl_all = nullptr;          // world × max(|S_r|) gathered switch lists
@@ -84,7 +90,11 @@ struct pg_game_s {
     // device-resident Algorithm 1 (pg_loop.cu): the instantiated graph and its capture stream
     cudaGraphExec_t loop_exec = nullptr;
     cudaStream_t cap_stream = nullptr;
-    bool device_loop = true;                  // PGSI_DEVICE_LOOP=0: the host-driven loop
+    // PGSI_DEVICE_LOOP: 0 = always the host-driven loop; 1 (default) = the device loop
+    // from the second pg_solve on a handle (building and instantiating the graph costs
+    // a few ms: a single solve is faster host-driven); 2 = always the device loop
+    int device_loop = 1;
+    int64_t solves = 0;                       // pg_solve calls on this handle
     int loop_nodes = 0;
 };
 
@@ -359,15 +369,55 @@ void note_valuation(pg_game h, bool full_rows, bool inc, bool bfs = false) {
 // then the lists (padded to the largest), compact the union into swl (it is S of
 // the next incremental step on every rank) and apply it. The host copies of the
 // counters become the global ones, so every rank takes the same decisions.
+#define NCK(h, x)                                                                        \
+    do {                                                                                 \
+        ncclResult_t r_ = (x);                                                           \
+        if (r_ != ncclSuccess) {                                                         \
+            set_err(std::string(#x) + ": " + ncclGetErrorString(r_));                    \
+            return PG_ENCCL;                                                             \
+        }                                                                                \
+    } while (0)
+
+bool dist_active(pg_game h) { return h->dist_fn != nullptr || h->nccl != nullptr; }
+
+// Communicators by ncclUniqueId: handles of one process that join with the same id
+// (e.g. a fresh pg_load per end-to-end step) share one communicator instead of
+// paying ncclCommInitRank again; destroyed with the last handle using it.
+struct CommEntry {
+    ncclComm_t comm;
+    int rank, world, device, refs;
+};
+std::mutex g_comm_mu;
+std::map<std::string, CommEntry> g_comms;
+
+void comm_release(ncclComm_t c) {
+    std::lock_guard<std::mutex> lk(g_comm_mu);
+    for (auto it = g_comms.begin(); it != g_comms.end(); ++it)
+        if (it->second.comm == c) {
+            if (--it->second.refs == 0) {
+                ncclCommDestroy(c);
+                g_comms.erase(it);
+            }
+            return;
+        }
+}
+
 pg_status dist_exchange(pg_game h, bool odd) {
-    if (!h->dist_fn) return PG_OK;
+    if (!dist_active(h)) return PG_OK;
     const double t0 = now_ms();
     const int W = h->dist_world;
     std::vector<int64_t> all(W);
-    h->h_x[0] = (int64_t)h->h_ctl->nswl;
-    if (h->dist_fn(h->dist_ctx, h->h_x, all.data(), sizeof(int64_t), 0)) {
-        set_err("pg_dist_attach: all-gather callback failed (switch-list sizes)");
-        return PG_ENCCL;
+    if (h->nccl) {   // NCCL on the handle's stream: sizes straight from the device counter
+        NCK(h, ncclAllGather(&h->G.ctl->nswl, h->d_cnts, 1, ncclUint64, h->nccl, h->stream));
+        CK(h, cudaMemcpyAsync(h->h_x + 4, h->d_cnts, sizeof(int64_t) * W, cudaMemcpyDeviceToHost, h->stream));
+        CK(h, cudaStreamSynchronize(h->stream));
+        for (int r = 0; r < W; r++) all[r] = h->h_x[4 + r];
+    } else {
+        h->h_x[0] = (int64_t)h->h_ctl->nswl;
+        if (h->dist_fn(h->dist_ctx, h->h_x, all.data(), sizeof(int64_t), 0)) {
+            set_err("pg_dist_attach: all-gather callback failed (switch-list sizes)");
+            return PG_ENCCL;
+        }
     }
     int64_t maxc = 0, total = 0;
     for (int r = 0; r < W; r++) { maxc = std::max(maxc, all[r]); total += all[r]; }
@@ -381,7 +431,9 @@ pg_status dist_exchange(pg_game h, bool odd) {
             CK(h, dalloc(h, &h->swl_all, cap));
             h->swl_all_cap = cap;
         }
-        if (h->dist_fn(h->dist_ctx, h->G.swl, h->swl_all, (int64_t)sizeof(int2) * maxc, 1)) {
+        if (h->nccl) {
+            NCK(h, ncclAllGather(h->G.swl, h->swl_all, (size_t)(2 * maxc), ncclInt32, h->nccl, h->stream));
+        } else if (h->dist_fn(h->dist_ctx, h->G.swl, h->swl_all, (int64_t)sizeof(int2) * maxc, 1)) {
             set_err("pg_dist_attach: all-gather callback failed (switch lists)");
             return PG_ENCCL;
         }
@@ -436,7 +488,7 @@ pg_status valuate_and_switch(pg_game h, bool odd, bool want_cdom, bool do_switch
     bool bfs = !inc && bfs_ok;
     const bool traced = do_switch && (h->flags & PG_TRACE);
     // sharded: the host exchanges S every step; traced: every valuation is hashed
-    if (h->dist_fn || h->G.trace_ts || traced) max_steps = 1;
+    if (dist_active(h) || h->G.trace_ts || traced) max_steps = 1;
     max_steps = std::min<int64_t>(max_steps, h->inc_max_steps);
     if (traced) {
         pg_status rc = trace_begin(h);
@@ -872,6 +924,7 @@ void pg_free(pg_game h) try {
         else cudaFree(p);
     }
     if (h->stream) cudaStreamSynchronize(h->stream);
+    if (h->nccl) comm_release(h->nccl);
     if (h->loop_exec) cudaGraphExecDestroy(h->loop_exec);
     if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
     if (h->h_ctl) cudaFreeHost(h->h_ctl);
@@ -1055,7 +1108,7 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     G.inc_grid_cap = h->lc.coop_inc;
     G.inc_grid_mul = getenv("PGSI_INC_GRID_MUL") ? atoi(getenv("PGSI_INC_GRID_MUL")) : 16;
     if (getenv("PGSI_SMALL_MAX")) h->small_max = atoll(getenv("PGSI_SMALL_MAX"));
-    if (getenv("PGSI_DEVICE_LOOP")) h->device_loop = atoi(getenv("PGSI_DEVICE_LOOP")) != 0;
+    if (getenv("PGSI_DEVICE_LOOP")) h->device_loop = atoi(getenv("PGSI_DEVICE_LOOP"));
     if (cudaDeviceGetAttribute(&h->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device) != cudaSuccess)
         h->smem_optin = 48 * 1024;
     G.inc_e_in_v2 = getenv("PGSI_INC_E_V2") ? atoi(getenv("PGSI_INC_E_V2")) : 1;
@@ -1151,6 +1204,10 @@ pg_status pg_dist_attach(pg_game h, int32_t rank, int32_t world, pg_allgather_fn
         a = lo + rank * q + std::min<int64_t>(rank, r);
         b = a + q + (rank < r ? 1 : 0);
     };
+    if (h->nccl) {   // a callback transport replaces the library's communicator
+        comm_release(h->nccl);
+        h->nccl = nullptr;
+    }
     if (world == 1 || !fn) {
         h->dist_fn = nullptr;
         h->dist_ctx = nullptr;
@@ -1167,6 +1224,70 @@ pg_status pg_dist_attach(pg_game h, int32_t rank, int32_t world, pg_allgather_fn
     }
     h->dist_fn = fn;
     h->dist_ctx = ctx;
+    h->dist_rank = rank;
+    h->dist_world = world;
+    span(0, G.n_even, G.sh_even_lo, G.sh_even_hi);
+    span(G.n_even, G.n_int - G.n_even, G.sh_odd_lo, G.sh_odd_hi);
+    G.sharded = 1;
+    return PG_OK;
+} PGSI_ABI_CATCH
+
+pg_status pg_dist_unique_id(void *id, int64_t bytes) try {
+    if (!id || bytes < (int64_t)sizeof(ncclUniqueId)) {
+        set_err("pg_dist_unique_id: need a buffer of " + std::to_string(sizeof(ncclUniqueId)) + " bytes");
+        return PG_EINVAL;
+    }
+    ncclUniqueId u;
+    NCK(nullptr, ncclGetUniqueId(&u));
+    std::memcpy(id, &u, sizeof(u));
+    return PG_OK;
+} PGSI_ABI_CATCH
+
+pg_status pg_dist_init(pg_game h, const void *id, int32_t rank, int32_t world) try {
+    pg_status rc = check_handle(h);
+    if (rc) return rc;
+    if (!id || world < 1 || rank < 0 || rank >= world) { set_err("pg_dist_init: need an id and 0 <= rank < world"); return PG_EINVAL; }
+    DeviceGuard dg(h->device);
+    if (h->nccl) {
+        comm_release(h->nccl);
+        h->nccl = nullptr;
+    }
+    h->dist_fn = nullptr;
+    h->dist_ctx = nullptr;
+    ncclUniqueId u;
+    std::memcpy(&u, id, sizeof(u));
+    CK(h, cudaStreamSynchronize(h->stream));
+    {
+        const std::string key((const char *)&u, sizeof(u));
+        std::lock_guard<std::mutex> lk(g_comm_mu);
+        auto it = g_comms.find(key);
+        if (it != g_comms.end()) {
+            if (it->second.rank != rank || it->second.world != world || it->second.device != h->device) {
+                set_err("pg_dist_init: this id is in use with another rank / world / device");
+                return PG_EINVAL;
+            }
+            it->second.refs++;
+            h->nccl = it->second.comm;
+        } else {
+            NCK(h, ncclCommInitRank(&h->nccl, world, u, rank));
+            g_comms[key] = CommEntry{h->nccl, rank, world, h->device, 1};
+        }
+    }
+    if (!h->h_x) CK(h, cudaMallocHost((void **)&h->h_x, sizeof(int64_t) * (4 + (size_t)world)));
+    else {
+        cudaFreeHost(h->h_x);
+        h->h_x = nullptr;
+        CK(h, cudaMallocHost((void **)&h->h_x, sizeof(int64_t) * (4 + (size_t)world)));
+    }
+    dfree(h, h->d_cnts);
+    h->d_cnts = nullptr;
+    CK(h, dalloc(h, &h->d_cnts, (size_t)world));
+    DevGame &G = h->G;
+    auto span = [&](int64_t lo, int64_t n, int64_t &a, int64_t &b) {   // balanced contiguous shard
+        const int64_t q = n / world, r = n % world;
+        a = lo + rank * q + std::min<int64_t>(rank, r);
+        b = a + q + (rank < r ? 1 : 0);
+    };
     h->dist_rank = rank;
     h->dist_world = world;
     span(0, G.n_even, G.sh_even_lo, G.sh_even_hi);
@@ -1269,7 +1390,7 @@ pg_status pg_solve(pg_game h, uint8_t *winner, int32_t *sigma, int32_t *tau, int
         }
         // the whole of Algorithm 1 in one single-block launch (pg_small.cu) when its state
         // fits in shared memory
-        const bool small = h->G.n_int + 1 <= h->small_max && !h->dist_fn &&
+        const bool small = h->G.n_int + 1 <= h->small_max && !dist_active(h) &&
                            !(h->flags & (PG_BELLMAN_FORD | PG_TRACE)) &&
                            small_scratch_bytes(h->G.n_int, h->G.dp, check) <= (size_t)h->smem_optin;
         if (small) {
@@ -1299,7 +1420,8 @@ pg_status pg_solve(pg_game h, uint8_t *winner, int32_t *sigma, int32_t *tau, int
         // Algorithm 1 on the device (pg_loop.cu) unless a host-side feature is on:
         // per-phase CUDA events, the trace, sharding, the BFS valuation, the
         // Bellman-Ford arm, or odd-cycle checks (cycle-dominant priorities)
-        const bool graph = !small && h->device_loop && !check && !h->dist_fn && !h->trace &&
+        const bool graph = !small && (h->device_loop == 2 || (h->device_loop == 1 && h->solves > 0)) && !check &&
+                           !dist_active(h) && !h->trace &&
                            !(h->flags & (PG_PHASE_TIMING | PG_TRACE | PG_BFS | PG_BELLMAN_FORD));
         if (graph) {
             PhaseScope ps(h, PH_OTHER);
@@ -1328,6 +1450,7 @@ pg_status pg_solve(pg_game h, uint8_t *winner, int32_t *sigma, int32_t *tau, int
     }
     h->st.inner_iters = inner;
     h->st.outer_passes = outer;
+    h->solves++;
     if (rc) { timing_collect(h); if (stats) *stats = h->st; return rc; }
     const int64_t n = h->n;
     std::vector<OutBuf> outs = {{winner, nullptr, (size_t)n},

@@ -5,9 +5,11 @@ One process per GPU, two modes:
 - replicas (default bench): every rank solves its own independent game (weak
   scaling); the only collectives are the bench's max-over-ranks timing and the
   sum of processed valuations;
-- sharded (``pg_dist_attach``): all ranks solve ONE game,
-  the valuation is replicated and the switch steps are split by vertex range;
-  the per-step switch lists travel through :func:`torch_allgather`.
+- sharded (the bench's default for N > 1): all ranks solve ONE
+  game, the valuation is replicated and the switch steps are split by vertex range.
+  With ``pg_dist_init`` the per-step switch lists travel through the library's own
+  NCCL communicator (:func:`nccl_join` only ships the ncclUniqueId); with
+  ``pg_dist_attach`` through a caller all-gather such as :func:`torch_allgather`.
 
 Works with the ``nccl`` backend on GPUs and ``gloo`` on CPU (tests).
 """
@@ -52,6 +54,33 @@ def shard_range(n: int, rank: int, world: int) -> Tuple[int, int]:
     q, r = divmod(n, world)
     lo = rank * q + min(rank, r)
     return lo, lo + q + (1 if rank < r else 0)
+
+
+def nccl_join(game_handle, dist, rank: int, world: int, nccl_id: bytes | None = None) -> bytes | None:
+    """Make a loaded ``Game`` one of `world` ranks of a sharded solve with the library's
+    own NCCL communicator: rank 0 creates the ncclUniqueId, torch.distributed
+    broadcasts its 128 bytes, every rank calls ``pg_dist_init``. Returns the id: passing
+    it again for another handle of the same ranks reuses the communicator."""
+    from .pg import dist_unique_id
+    if world < 1 or (dist is None and world > 1):
+        raise ValueError("nccl_join: world > 1 needs a torch.distributed process group")
+    if nccl_id is None:
+        obj = [dist_unique_id() if rank == 0 else None]
+        if dist is not None:
+            dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    game_handle.dist_init(nccl_id, rank, world)
+    return nccl_id
+
+
+def reduce_max(dist, x: float, device=None) -> float:
+    """Max over ranks (no-op on one process)."""
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
 
 
 def reduce_time_and_units(dist, ms: float, units: float, device=None) -> Tuple[float, float]:

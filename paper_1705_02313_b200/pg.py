@@ -96,10 +96,12 @@ def load_library(path: str = LIB_PATH):
     L.pg_solve.argtypes = [C.c_void_p, P, P, P, P, C.POINTER(Stats)]
     L.pg_get_stats.argtypes = [C.c_void_p, C.POINTER(Stats)]
     L.pg_get_trace.argtypes = [C.c_void_p, P, C.c_int64, P]
+    L.pg_dist_unique_id.argtypes = [P, C.c_int64]
+    L.pg_dist_init.argtypes = [C.c_void_p, P, C.c_int32, C.c_int32]
     L.pg_inspect.argtypes = [C.c_int64, P, P, P, P, C.c_uint32] + [P] * 9
     L.pg_dist_attach.argtypes = [C.c_void_p, C.c_int32, C.c_int32, ALLGATHER_FN, P]
     for f in ("pg_load", "pg_info", "pg_valuate", "pg_best_response", "pg_solve", "pg_get_stats",
-              "pg_inspect", "pg_dist_attach", "pg_get_trace"):
+              "pg_inspect", "pg_dist_attach", "pg_get_trace", "pg_dist_unique_id", "pg_dist_init"):
         getattr(L, f).restype = C.c_int
     L.pg_parse_pgsolver.argtypes = [C.c_char_p, C.c_int64, P, P, P, P, P, P]
     L.pg_format_solution.argtypes = [C.c_int64, P, P, P, P, C.c_char_p, C.c_int64, P]
@@ -222,6 +224,12 @@ class Game:
         self.dist_error = None
         self._check(_lib.pg_dist_attach(self._h, int(rank), int(world), self._dist_cb, None))
 
+    def dist_init(self, nccl_id: bytes, rank: int, world: int):
+        """Join `world` ranks solving this same game with the library's own NCCL
+        communicator (``pg_dist_init``); ``nccl_id`` from :func:`dist_unique_id` on rank 0."""
+        buf = C.create_string_buffer(bytes(nccl_id), len(nccl_id))
+        self._check(_lib.pg_dist_init(self._h, buf, int(rank), int(world)))
+
     def stats(self) -> dict:
         s = Stats()
         self._check(_lib.pg_get_stats(self._h, C.byref(s)))
@@ -296,6 +304,16 @@ def inspect(g, preprocess: bool = True):
         raise PGError(rc, L.pg_last_error().decode())
     return dict(n_internal=ni.value, d=d.value, dummies=du.value, owner=owner, pidx=pidx,
                 adj_ptr=adj_ptr, adj=adj[:mi.value], priorities=pri[:d.value])
+
+
+def dist_unique_id() -> bytes:
+    """A fresh ncclUniqueId (128 bytes) for :meth:`Game.dist_init` (``pg_dist_unique_id``)."""
+    L = load_library()
+    buf = C.create_string_buffer(128)
+    rc = L.pg_dist_unique_id(buf, 128)
+    if rc:
+        raise PGError(rc, L.pg_last_error().decode())
+    return buf.raw
 
 
 def version() -> str:

@@ -35,6 +35,7 @@ def same(r, ora, n):
 @pytest.mark.parametrize("seed", range(10))
 def test_device_loop_matches_oracle_and_host_loop(pg, monkeypatch, seed):
     monkeypatch.setenv("PGSI_SMALL_MAX", "0")
+    monkeypatch.setenv("PGSI_DEVICE_LOOP", "2")
     rng = np.random.default_rng(700 + seed)
     n = int(rng.integers(20_000, 300_000))
     d = int(rng.integers(2, 33))
@@ -54,6 +55,7 @@ def test_device_loop_matches_oracle_and_host_loop(pg, monkeypatch, seed):
 @pytest.mark.parametrize("fam", ["ladder", "elevator", "deep", "oddchain", "stair"])
 def test_device_loop_structured(pg, monkeypatch, fam):
     monkeypatch.setenv("PGSI_SMALL_MAX", "0")
+    monkeypatch.setenv("PGSI_DEVICE_LOOP", "2")
     g = {"ladder": lambda: gi.ladder(60_000, 2), "elevator": lambda: gi.elevator(12, 10, 1),
          "deep": lambda: gi.f_deep(50_000), "oddchain": lambda: gi.f_oddchain(3_000),
          "stair": lambda: gi.f_stair(3_000)}[fam]()
@@ -65,6 +67,7 @@ def test_device_loop_structured(pg, monkeypatch, fam):
 
 def test_device_loop_si_reset_and_caps(pg, monkeypatch):
     monkeypatch.setenv("PGSI_SMALL_MAX", "0")
+    monkeypatch.setenv("PGSI_DEVICE_LOOP", "2")
     g = gi.random_game(80_000, 12, 2, 5, 4)
     ora = Oracle(g).solve(mode="si_reset")
     r = pg.Game.from_game(g, best_response="si_reset").solve(want_val=True)
@@ -73,14 +76,28 @@ def test_device_loop_si_reset_and_caps(pg, monkeypatch):
     full = Oracle(g).solve()
     for kw in (dict(max_outer=2), dict(max_inner=3), dict(max_inner=full.inner_iters - 1),
                dict(max_outer=full.outer_passes - 1)):
-        for loop in ("1", "0"):
+        for loop in ("2", "0"):
             monkeypatch.setenv("PGSI_DEVICE_LOOP", loop)
             with pytest.raises(pg.PGError) as e:
                 pg.Game.from_game(g, **kw).solve()
             assert e.value.name == "PG_EITERCAP", (kw, loop)
-    monkeypatch.setenv("PGSI_DEVICE_LOOP", "1")
+    monkeypatch.setenv("PGSI_DEVICE_LOOP", "2")
     r = pg.Game.from_game(g, max_inner=full.inner_iters, max_outer=full.outer_passes).solve(want_val=True)
     same(r, full, g.n)
+
+
+def test_device_loop_default_policy(pg, monkeypatch):
+    """Default (PGSI_DEVICE_LOOP unset): the first pg_solve of a handle runs the
+    host-driven loop, later ones the graph; all equal."""
+    monkeypatch.setenv("PGSI_SMALL_MAX", "0")
+    monkeypatch.delenv("PGSI_DEVICE_LOOP", raising=False)
+    g = gi.random_game(90_000, 16, 2, 5, 6)
+    ora = Oracle(g).solve()
+    G = pg.Game.from_game(g)
+    rs = [G.solve(want_val=True) for _ in range(3)]
+    assert [r.stats["device_loop_solves"] for r in rs] == [0, 1, 1]
+    for r in rs:
+        same(r, ora, g.n)
 
 
 def test_device_loop_splitter_growth(pg, monkeypatch):
@@ -88,6 +105,7 @@ def test_device_loop_splitter_growth(pg, monkeypatch):
     buffers hold. The graph ends with LS_HOST_SPLITTERS; the host grows the buffers,
     rebuilds the graph and resumes."""
     monkeypatch.setenv("PGSI_SMALL_MAX", "0")
+    monkeypatch.setenv("PGSI_DEVICE_LOOP", "2")
     L = 100_000
     owner = [0] + [1] * L
     prio = [2] + [1] * L
@@ -107,7 +125,7 @@ def test_device_loop_epoch_wrap(pg, monkeypatch):
     ora = Oracle(g).solve()
     for start in ("0xffffff00", "0xfffffffa"):
         monkeypatch.setenv("PGSI_EPOCH_START", start)
-        for loop in ("1", "0"):
+        for loop in ("2", "0"):
             monkeypatch.setenv("PGSI_DEVICE_LOOP", loop)
             r = pg.Game.from_game(g).solve(want_val=True)
             same(r, ora, g.n)

@@ -237,3 +237,55 @@ def test_sharded_solve_processes_gloo(pg):
         np.testing.assert_array_equal(np.frombuffer(s, np.int32), ora.sigma)
         np.testing.assert_array_equal(np.frombuffer(t, np.int32), ora.tau)
         np.testing.assert_array_equal(np.frombuffer(v, np.int32).reshape(ora.val.shape), ora.val)
+
+
+# ------------------------------------------------- the library's own NCCL (pg_dist_init)
+@pytest.mark.parametrize("seed", range(3))
+def test_nccl_dist_init_world1_matches_oracle(pg, seed, monkeypatch):
+    """pg_dist_init with a fresh ncclUniqueId at world = 1: the sharded code path runs
+    end to end through NCCL inside libpgsi (sizes and switch lists all-gathered on the
+    handle's stream after every switch step, then applied), bit-identical to the
+    oracle. One GPU per rank is an NCCL requirement, so world > 1 needs more GPUs; the
+    exchange protocol itself is the one the W = 2..4 tests above exercise."""
+    monkeypatch.setenv("PGSI_SMALL_MAX", "0")
+    g = gi.random_game(60_000 + 20_000 * seed, 8 + 8 * seed, 2, 5, seed)
+    ora = Oracle(g).solve()
+    nid = pg.dist_unique_id()
+    assert len(nid) == 128
+    G = pg.Game.from_game(g)
+    G.dist_init(nid, 0, 1)
+    r = G.solve(want_val=True)
+    assert r.stats["dist_exchanges"] > 0 and r.stats["device_loop_solves"] == 0
+    assert r.stats["inner_iters"] == ora.inner_iters and r.stats["outer_passes"] == ora.outer_passes
+    np.testing.assert_array_equal(r.winner, ora.winner)
+    np.testing.assert_array_equal(r.sigma, ora.sigma)
+    np.testing.assert_array_equal(r.tau, ora.tau)
+    np.testing.assert_array_equal(r.val.reshape(g.n, -1), ora.val)
+    # a second handle with the same id shares the communicator; both stay usable
+    G2 = pg.Game.from_game(g)
+    G2.dist_init(nid, 0, 1)
+    r2 = G2.solve()
+    np.testing.assert_array_equal(r2.tau, ora.tau)
+    G.free()
+    r3 = G2.solve()
+    np.testing.assert_array_equal(r3.sigma, ora.sigma)
+    G2.free()
+
+
+def test_nccl_dist_init_errors(pg):
+    g = gi.random_game(5000, 4, 2, 5, 1)
+    G = pg.Game.from_game(g)
+    nid = pg.dist_unique_id()
+    for rank, world in ((1, 1), (-1, 2), (0, 0)):
+        with pytest.raises(pg.PGError) as e:
+            G.dist_init(nid, rank, world)
+        assert e.value.name == "PG_EINVAL"
+    G.dist_init(nid, 0, 1)
+    G2 = pg.Game.from_game(g)
+    with pytest.raises(pg.PGError) as e:   # the same id cannot mean another rank / world
+        G2.dist_init(nid, 0, 2)
+    assert e.value.name == "PG_EINVAL"
+    # detaching returns to the single-GPU device loop
+    G.attach_dist(0, 1)
+    G.solve()
+    assert G.solve().stats["device_loop_solves"] == 1

@@ -55,11 +55,15 @@ def first_divergence(gpu_trace, ora_trace):
 
 
 def bench_solve(pg, g):
-    """One pg_solve in bench.py's launch configuration; host numpy outputs."""
+    """pg_solve in bench.py's timed configuration (device pointers on torch's current
+    stream; a warm handle, so Algorithm 1 runs as the device-resident graph); host
+    numpy outputs of the second solve."""
     import torch
     stream = torch.cuda.current_stream(torch.device("cuda", 0))
-    G = pg.Game.from_game(g, device=0, stream=stream.cuda_stream, device_ptrs=True, phase_timing=True)
+    G = pg.Game.from_game(g, device=0, stream=stream.cuda_stream, device_ptrs=True)
+    G.solve()
     res = G.solve(want_val=True)
+    assert res.stats["device_loop_solves"] == 1
     torch.cuda.synchronize()
     out = dict(winner=res.winner.cpu().numpy(), sigma=res.sigma.cpu().numpy(), tau=res.tau.cpu().numpy(),
                val=res.val.cpu().numpy(), stats=res.stats)
