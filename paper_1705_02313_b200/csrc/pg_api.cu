@@ -1087,6 +1087,10 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     CKL(dalloc(h, &G.Dl, N1));
     CKL(dalloc(h, &G.Dr, N1));
     CKL(dalloc(h, &G.El, N1));
+    for (int b = 0; b < 2; b++) {
+        CKL(dalloc(h, &G.Ol[b], N1));
+        CKL(dalloc(h, &G.Or[b], N1));
+    }
     CKL(dalloc(h, &G.Cl, N1));
     CKL(cudaMemsetAsync(G.dmark, 0, sizeof(uint32_t) * N1, s));
     CKL(cudaMemsetAsync(G.emark, 0, sizeof(uint32_t) * N1, s));
@@ -1115,6 +1119,8 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     G.inc_fuse_e = getenv("PGSI_INC_FUSE_E") ? atoi(getenv("PGSI_INC_FUSE_E")) : 0;   // measured slower
     G.inc_skip_v1 = getenv("PGSI_INC_SKIP_V1") ? atoi(getenv("PGSI_INC_SKIP_V1")) : 1;
     G.inc_blk_frontier = getenv("PGSI_INC_BLK") ? atoi(getenv("PGSI_INC_BLK")) : 256;
+    G.inc_closure = getenv("PGSI_INC_CLOSURE") ? atoi(getenv("PGSI_INC_CLOSURE")) : 1;
+    G.inc_clo_cap = getenv("PGSI_INC_CLO_CAP") ? std::max(1, atoi(getenv("PGSI_INC_CLO_CAP"))) : 1 << 30;
     G.lvlog = nullptr;
     if (trace_levels) {
         CKL(dalloc(h, &G.lvlog, 8192));

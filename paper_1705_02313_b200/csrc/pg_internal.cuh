@@ -30,6 +30,7 @@ namespace pgsi {
 
 constexpr int kMaxD = 256;       // pidx is uint8
 constexpr int kThreads = 256;
+constexpr int kIncThreads = 512;   // k_inc_iter block size (one 512-thread block per SM at 128 registers)
 
 // Per-valuation / per-call device counters (one block of device memory).
 struct Ctl {
@@ -64,6 +65,7 @@ struct Ctl {
     unsigned long long nD_sum;      // ... |D| summed over its steps
     unsigned long long nE_sum;      // ... |E| summed over its steps
     unsigned long long cpx_gathers; // switch steps: 32 B prefix gathers after an undecided key compare
+    unsigned long long nDl;         // incremental step: D-list length (block-local closure appends)
     // ---- not reset per valuation ----
     unsigned long long bad_index;   // ULLONG_MAX = none, else min invalid ABI index
     unsigned long long nhard;       // vertices deferred to the hard (full-compare) pass
@@ -129,6 +131,8 @@ struct DevGame {
     int32_t *Dl;        // D list
     uint2 *Dr;          // reverse-CSR range [rrp[v], rrp[v+1]) of each D-list entry
     int32_t *El;        // E list
+    int32_t *Ol[2];     // block-local closure: overflow root lists (double-buffered) ...
+    uint2 *Or[2];       // ... with their reverse-CSR ranges
     uint32_t *cmark;    // epoch marks: v in C
     int32_t *Cl;        // C list
     int32_t inc_max_levels;   // abort the incremental step beyond this closure depth
@@ -163,6 +167,8 @@ struct DevGame {
     int32_t inc_e_in_v2;    // build E in the V2-on-D pass (else a separate pass)
     int32_t inc_skip_v1;    // after All_Odd steps replace V1 on D by the V2 walk depth
     int32_t inc_blk_frontier; // closure levels with at most this many frontier vertices run in block 0
+    int32_t inc_closure;      // 1 = block-local closure phases (closure_block), 0 = level-synchronous BFS
+    int32_t inc_clo_cap;      // closure_block frontier capacity in use (<= kCloCap; testing shrinks it)
 };
 
 struct LaunchCfg {

@@ -1100,13 +1100,34 @@ __device__ __forceinline__ void warp_append8(const int32_t (&u)[8], const bool (
 template <int MODE>
 __device__ __forceinline__ void expand_rev(const DevGame &g, int32_t f, uint32_t rb, uint32_t re, uint32_t *mark,
                                            uint32_t ep, int32_t *out, unsigned long long *cnt) {
-    const int maxd = (int)__reduce_max_sync(FULL, re - rb);
-    for (int k0 = 0; k0 < maxd; k0 += 8) {
+    static_assert(MODE == 1 || MODE == 2, "expand_rev: MODE 1 (Odd) or 2 (Even)");
+    // edge-parallel over the warp's reverse edges (as closure_block): 8 edges per lane
+    // per round, the loads and mark exchanges of a round issued together
+    const int lane = threadIdx.x & 31;
+    const uint32_t deg = re - rb;
+    uint32_t incl_d = deg;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(FULL, incl_d, o);
+        if (lane >= o) incl_d += t;
+    }
+    const uint32_t excl_d = incl_d - deg;
+    const uint32_t E = __shfl_sync(FULL, incl_d, 31);
+    for (uint32_t e0 = 0; e0 < E; e0 += 32 * 8) {
         int32_t u[8];
         bool ok[8];
 #pragma unroll
-        for (int j = 0; j < 8; j++) u[j] = (rb + k0 + j < re) ? __ldg(g.rcol + rb + k0 + j) : -1;
-        static_assert(MODE == 1 || MODE == 2, "expand_rev: MODE 1 (Odd) or 2 (Even)");
+        for (int j = 0; j < 8; j++) {
+            const uint32_t e = e0 + (uint32_t)j * 32 + lane;
+            int o = 0;
+#pragma unroll
+            for (int st = 16; st; st >>= 1) {
+                const uint32_t x = __shfl_sync(FULL, excl_d, o + st);
+                if (o + st < 32 && x <= e) o += st;
+            }
+            const uint32_t ro = __shfl_sync(FULL, rb, o), xo = __shfl_sync(FULL, excl_d, o);
+            u[j] = e < E ? __ldg(g.rcol + ro + (e - xo)) : -1;
+        }
         if constexpr (MODE == 1) {
 #pragma unroll
             for (int j = 0; j < 8; j++) ok[j] = u[j] >= 0 && u[j] >= g.n_even;
@@ -1200,6 +1221,197 @@ __device__ __forceinline__ void trace_level(const DevGame &g, int64_t width, int
     }
 }
 
+// Block-local dirty closure (step 1 of k_inc_iter, PGSI_INC_CLOSURE=1, default).
+// D is a union of subtrees of the reversed functional graph hanging below S: a
+// vertex u joins because succ(u) is in D, and it is discovered exactly once, by its
+// successor (only members of S, marked before the first phase, can be met twice).
+// Subtrees are therefore independent, and a block expands the subtrees of its share
+// of the roots level by level in SHARED memory, with __syncthreads between levels and
+// no grid barrier: a level costs two dependent loads (reverse edges, then the
+// children's succ / mark / range). A block frontier holds kCloCap vertices; children
+// beyond it go to a global overflow list (and the D list) and are the roots of the
+// next phase, which every block shares again after one grid barrier. New D vertices
+// are staged in shared memory and flushed to the D list with one atomic per block.
+constexpr int kCloCap = 2048;      // block frontier capacity (vertices)
+constexpr int kCloStage = 4096;    // D-list staging capacity (vertices)
+constexpr size_t kCloSmem = (size_t)(2 * kCloCap + kCloStage) * (sizeof(int32_t) + sizeof(uint2));
+
+// Expand the roots (Rv, Rr)[lo, hi) of this block; returns false if the level cap hit.
+__device__ bool closure_block(const DevGame &g, const int32_t *Rv, const uint2 *Rr, int64_t lo, int64_t hi,
+                              uint32_t ep, int32_t *Ov, uint2 *Or, unsigned long long *ocnt, int &maxlev) {
+    extern __shared__ __align__(16) unsigned char clo_smem[];
+    uint2 *fr = reinterpret_cast<uint2 *>(clo_smem);                 // [2][kCloCap]
+    uint2 *sr = fr + 2 * kCloCap;                                    // [kCloStage]
+    int32_t *fv = reinterpret_cast<int32_t *>(sr + kCloStage);       // [2][kCloCap]
+    int32_t *sv = fv + 2 * kCloCap;                                  // [kCloStage]
+    __shared__ unsigned int s_cnt[2], s_stage;
+    __shared__ int s_abort;
+    const int lane = threadIdx.x & 31;
+    Ctl *ctl = g.ctl;
+    // capacities in use (PGSI_INC_CLO_CAP shrinks them to exercise the overflow paths)
+    const unsigned int FC = (unsigned int)min(kCloCap, g.inc_clo_cap), SC = min((unsigned int)kCloStage, 2u * FC);
+    if (threadIdx.x == 0) { s_stage = 0; s_abort = 0; }
+    bool ok_all = true;
+    for (int64_t base = lo; base < hi; base += FC) {
+        const int k = (int)min((int64_t)FC, hi - base);
+        __syncthreads();
+        for (int i = threadIdx.x; i < k; i += blockDim.x) {
+            fv[i] = __ldcg(Rv + base + i);
+            fr[i] = __ldcg(Rr + base + i);
+        }
+        int nf = k, cur = 0, lev = 0;
+        while (nf > 0) {
+            lev++;
+            unsigned int *cnt = &s_cnt[lev & 1];
+            if (threadIdx.x == 0) *cnt = 0;
+            __syncthreads();
+            const int32_t *cv = fv + cur * kCloCap;
+            const uint2 *cr = fr + cur * kCloCap;
+            int32_t *nv = fv + (cur ^ 1) * kCloCap;
+            uint2 *nr = fr + (cur ^ 1) * kCloCap;
+            for (int b0 = threadIdx.x - lane; b0 < nf; b0 += blockDim.x) {   // warp-uniform
+                const int i = b0 + lane;
+                int32_t f = -1;
+                uint32_t rb = 0, re = 0;
+                if (i < nf) {
+                    f = cv[i];
+                    rb = cr[i].x;
+                    re = cr[i].y;
+                }
+                // Edge-parallel expansion: the warp's reverse edges form one flat list
+                // (exclusive scan of the degrees), each lane takes EB edges per round,
+                // finds its edge's frontier vertex by a binary search over the lanes'
+                // offsets, and issues all loads of the round together: a round is two
+                // dependent loads however uneven the degrees (a lane-per-vertex loop
+                // costs two per 8 edges of the warp's largest degree).
+                constexpr int EB = 4;
+                const uint32_t deg = f >= 0 ? re - rb : 0u;
+                uint32_t incl_d = deg;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t t = __shfl_up_sync(FULL, incl_d, o);
+                    if (lane >= o) incl_d += t;
+                }
+                const uint32_t excl_d = incl_d - deg;
+                const uint32_t E = __shfl_sync(FULL, incl_d, 31);
+                for (uint32_t e0 = 0; e0 < E; e0 += 32 * EB) {
+                    int32_t u[EB], par[EB], su[EB];
+                    uint32_t mk[EB], ub[EB], ue[EB];
+                    bool ok[EB];
+#pragma unroll
+                    for (int j = 0; j < EB; j++) {
+                        const uint32_t e = e0 + (uint32_t)j * 32 + lane;
+                        int o = 0;   // last lane whose offset is <= e (it owns edge e)
+#pragma unroll
+                        for (int st = 16; st; st >>= 1) {
+                            const uint32_t x = __shfl_sync(FULL, excl_d, o + st);
+                            if (o + st < 32 && x <= e) o += st;
+                        }
+                        const int32_t fo = __shfl_sync(FULL, f, o);
+                        const uint32_t ro = __shfl_sync(FULL, rb, o), xo = __shfl_sync(FULL, excl_d, o);
+                        par[j] = fo;
+                        u[j] = e < E ? __ldg(g.rcol + ro + (e - xo)) : -1;
+                    }
+#pragma unroll
+                    for (int j = 0; j < EB; j++) {   // all loads of the round issued together
+                        const int32_t x = u[j] >= 0 ? u[j] : 0;
+                        su[j] = __ldcg(g.succ + x);
+                        mk[j] = __ldcg(g.dmark + x);
+                        ub[j] = __ldg(g.rrp + x);
+                        ue[j] = __ldg(g.rrp + x + 1);
+                    }
+                    if (g.inc_fuse_e) {
+                        bool oe[8];
+                        int32_t uu[8];
+#pragma unroll
+                        for (int j = 0; j < 8; j++) {
+                            uu[j] = j < EB ? u[j] : -1;
+                            oe[j] = j < EB && u[j] >= 0 && u[j] >= g.n_even && atomicExch(g.emark + u[j], ep) != ep;
+                        }
+                        warp_append8(uu, oe, g.El, &ctl->nE);
+                    }
+                    int c = 0;
+#pragma unroll
+                    for (int j = 0; j < EB; j++) {
+                        ok[j] = u[j] >= 0 && su[j] == par[j] && mk[j] != ep;
+                        c += ok[j];
+                    }
+                    int incl = c;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int t = __shfl_up_sync(FULL, incl, o);
+                        if (lane >= o) incl += t;
+                    }
+                    const int total = __shfl_sync(FULL, incl, 31);
+                    if (total == 0) continue;
+                    unsigned int fbase = 0, sbase = 0;
+                    if (lane == 31) {
+                        fbase = atomicAdd(cnt, (unsigned int)total);
+                        sbase = atomicAdd(&s_stage, (unsigned int)total);
+                    }
+                    fbase = __shfl_sync(FULL, fbase, 31);
+                    sbase = __shfl_sync(FULL, sbase, 31);
+                    // entries past the frontier / staging capacity go to the global lists
+                    const int fover = (int)min((unsigned int)total, fbase + total > FC ? fbase + total - FC : 0u);
+                    const int sover = (int)min((unsigned int)total, sbase + total > SC ? sbase + total - SC : 0u);
+                    unsigned long long obase = 0, dbase = 0;
+                    if (lane == 31 && fover) obase = atomicAdd(ocnt, (unsigned long long)fover);
+                    if (lane == 31 && sover) dbase = atomicAdd(&ctl->nDl, (unsigned long long)sover);
+                    obase = __shfl_sync(FULL, obase, 31);
+                    dbase = __shfl_sync(FULL, dbase, 31);
+                    int pos = incl - c;   // this lane's first entry within the warp's round
+#pragma unroll
+                    for (int j = 0; j < EB; j++) {
+                        if (!ok[j]) continue;
+                        g.dmark[u[j]] = ep;
+                        const uint2 r = make_uint2(ub[j], ue[j]);
+                        const unsigned int fp = fbase + pos, sp = sbase + pos;
+                        if (fp < FC) {
+                            nv[fp] = u[j];
+                            nr[fp] = r;
+                        } else {
+                            const unsigned long long q = obase + (fp - max(fbase, FC));
+                            Ov[q] = u[j];
+                            Or[q] = r;
+                        }
+                        if (sp < SC) {
+                            sv[sp] = u[j];
+                            sr[sp] = r;
+                        } else {
+                            const unsigned long long q = dbase + (sp - max(sbase, SC));
+                            g.Dl[q] = u[j];
+                            g.Dr[q] = r;
+                        }
+                        pos++;
+                    }
+                }
+            }
+            __syncthreads();
+            nf = (int)min(*cnt, FC);
+            cur ^= 1;
+            if (threadIdx.x == 0 && lev > 24) trace_level(g, (int64_t)blockIdx.x << 16 | nf, lev, true);
+            if (lev >= g.inc_max_levels) {
+                if (threadIdx.x == 0) s_abort = 1;
+                break;
+            }
+        }
+        maxlev = max(maxlev, lev);
+        __syncthreads();
+        if (s_abort) { ok_all = false; break; }
+    }
+    // flush the staged D vertices: one atomic per block
+    __syncthreads();
+    const unsigned int ns_ = min(s_stage, SC);
+    __shared__ unsigned long long s_dbase;
+    if (threadIdx.x == 0 && ns_) s_dbase = atomicAdd(&ctl->nDl, (unsigned long long)ns_);
+    __syncthreads();
+    for (unsigned int i = threadIdx.x; i < ns_; i += blockDim.x) {
+        g.Dl[s_dbase + i] = sv[i];
+        g.Dr[s_dbase + i] = sr[i];
+    }
+    return ok_all;
+}
+
 __device__ __forceinline__ void trace_ts(const DevGame &g, int k) {
     if (g.trace_ts && blockIdx.x == 0 && threadIdx.x == 0) {
         unsigned long long t;
@@ -1208,9 +1420,9 @@ __device__ __forceinline__ void trace_ts(const DevGame &g, int k) {
     }
 }
 
-__global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
-    __shared__ uint8_t hsm[kThreads][36];
-    __shared__ uint32_t osm[kThreads][9];
+__global__ void __launch_bounds__(kIncThreads) k_inc_iter(DevGame g) {
+    __shared__ uint8_t hsm[kIncThreads][36];
+    __shared__ uint32_t osm[kIncThreads][9];
     const int64_t N = g.n_int;
     const uint32_t SINK = (uint32_t)N;
     const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -1236,10 +1448,45 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
         g.Dl[i] = v;
         g.Dr[i] = make_uint2(__ldg(g.rrp + v), __ldg(g.rrp + v + 1));
     }
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->nDl = (unsigned long long)ns;
     gbar(ctl);
     if (blockIdx.x == 0 && threadIdx.x == 0) { ctl->nswl = 0; ctl->nhard = 0; }  // step 5 appends anew
     int64_t lo = 0, hi = ns;
     int levels = 0;
+    if (g.inc_closure == 1) {
+        // block-local phases (closure_block); roots: S, then the overflow lists
+        int phase = 0, maxlev = 0;
+        const int32_t *Rv = g.Dl;
+        const uint2 *Rr = g.Dr;
+        int64_t nr = ns;
+        for (;;) {
+            unsigned long long *ocnt = &ctl->dcnt[phase % 3];   // reset two phases ahead
+            int32_t *Ov = g.Ol[phase & 1];
+            uint2 *Or = g.Or[phase & 1];
+            const int64_t per = (nr + gridDim.x - 1) / gridDim.x;
+            const int64_t blo = min(nr, (int64_t)blockIdx.x * per), bhi = min(nr, blo + per);
+            if (!closure_block(g, Rv, Rr, blo, bhi, ep, Ov, Or, ocnt, maxlev) && threadIdx.x == 0)
+                atomicOr(&ctl->inc_overflow, 1ull);
+            gbar(ctl);
+            nr = (int64_t)bcast_ld(ocnt);
+            hi = (int64_t)bcast_ld(&ctl->nDl);
+            const bool abort = bcast_ld(&ctl->inc_overflow) != 0 || hi > g.inc_max_dirty;
+            if (blockIdx.x == 0 && threadIdx.x == 0) ctl->dcnt[(phase + 2) % 3] = 0;
+            if (threadIdx.x == 0) atomicMax(&ctl->dlevels, (unsigned long long)maxlev);
+            if (abort) {
+                // deep or huge closure: a from-scratch valuation is cheaper. Nothing but
+                // marks (epoch-scoped) has been written; the host redoes the step in full.
+                if (blockIdx.x == 0 && threadIdx.x == 0) { ctl->inc_overflow = 1; ctl->nD = (unsigned long long)hi; }
+                return;
+            }
+            if (nr == 0) break;
+            Rv = Ov;
+            Rr = Or;
+            phase++;
+        }
+        levels = (int)bcast_ld(&ctl->dlevels);
+        lo = hi;   // the level-synchronous loop below is skipped
+    }
     // The per-level append counters rotate on the count of GRID levels (glev), which
     // the block-0 thin-frontier mode below never advances and never touches: a block
     // released late from the last grid level's barrier may still be reading
@@ -1530,7 +1777,7 @@ __global__ void __launch_bounds__(kThreads) k_inc_iter(DevGame g) {
         ctl->newfin[0] = ctl->newfin[1] = ctl->newfin[2] = 0;
         ctl->nE = 0;
     }
-    const int64_t need = (nsn * g.inc_grid_mul + kThreads - 1) / kThreads;   // the grid the host would pick
+    const int64_t need = (nsn * g.inc_grid_mul + kIncThreads - 1) / kIncThreads;   // the grid the host would pick
     if (sw == 0 || step + 1 >= (int)max_steps || nsn * g.inc_s_div > N ||
         (need > (int64_t)gridDim.x && (int)gridDim.x < g.inc_grid_cap))
         return;
@@ -1820,9 +2067,11 @@ cudaError_t setup_launch_cfg(LaunchCfg &lc, int device) {
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_val_bfs, kThreads, 0);
     if (e) return e;
     lc.coop_bfs = std::min(nb, 4) * lc.sms;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_inc_iter, kThreads, 0);
+    e = cudaFuncSetAttribute(k_inc_iter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCloSmem);
     if (e) return e;
-    lc.coop_inc = std::min(nb, 4) * lc.sms;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_inc_iter, kIncThreads, kCloSmem);
+    if (e) return e;
+    lc.coop_inc = std::min(nb, 2) * lc.sms;
     g_lc = lc;
     return cudaSuccess;
 }
@@ -1960,11 +2209,11 @@ cudaError_t launch_even_inc(const DevGame &g, cudaStream_t s) {
 }
 
 cudaError_t launch_inc_iter(const DevGame &g, const LaunchCfg &lc, cudaStream_t s, int64_t nS) {
-    int64_t grid = (nS * (int64_t)g.inc_grid_mul + kThreads - 1) / kThreads;   // as k_inc_iter's step 8 rule
+    int64_t grid = (nS * (int64_t)g.inc_grid_mul + kIncThreads - 1) / kIncThreads;   // as k_inc_iter's step 8 rule
     grid = std::max<int64_t>(1, std::min<int64_t>(grid, lc.coop_inc));
     DevGame gg = g;
     void *args[] = {&gg};
-    return cudaLaunchCooperativeKernel((const void *)k_inc_iter, dim3((unsigned)grid), dim3(kThreads), args, 0, s);
+    return cudaLaunchCooperativeKernel((const void *)k_inc_iter, dim3((unsigned)grid), dim3(kIncThreads), args, kCloSmem, s);
 }
 
 __global__ void k_set_launch_params(Ctl *ctl, uint32_t epoch, uint32_t cepoch, uint32_t s_odd, uint32_t max_steps) {

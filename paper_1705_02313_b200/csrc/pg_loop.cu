@@ -126,7 +126,7 @@ __global__ void k_inner_pre(LoopCfg cfg, Ctl *c, Handles h) {
         c->lp_cepoch = c->ls_cepoch;
         c->lp_s_odd = c->ls_last_sw_odd;
         c->lp_max_steps = (unsigned int)steps;
-        const long long need = ((long long)nsw * cfg.inc_grid_mul + kThreads - 1) / kThreads;
+        const long long need = ((long long)nsw * cfg.inc_grid_mul + kIncThreads - 1) / kIncThreads;
         mode = LM_INC3;
         for (int k = 0; k < 4; k++)
             if (need <= cfg.grid_class[k]) { mode = (unsigned int)k; break; }
@@ -360,7 +360,7 @@ cudaError_t build_loop_graph(const DevGame &g, const LaunchCfg &lc, const LoopCf
     const std::vector<cudaGraph_t> mb = b;
     const int omit = getenv("PGSI_LOOP_OMIT") ? atoi(getenv("PGSI_LOOP_OMIT")) : 0;   // debugging
     for (int k = 0; k < 4 && !(omit & 1); k++) {   // incremental launches, one grid class each
-        const int64_t nS = (int64_t)cfg.grid_class[k] * kThreads / std::max(1, cfg.inc_grid_mul);
+        const int64_t nS = (int64_t)cfg.grid_class[k] * kIncThreads / std::max(1, cfg.inc_grid_mul);
         GCK(capture(cs, mb[k], [&] { return launch_inc_iter(g, lc, cs, std::max<int64_t>(1, nS)); }));
     }
     GCK(capture(cs, mb[LM_FULL], [&] {

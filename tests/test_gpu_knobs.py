@@ -42,6 +42,10 @@ def check(pg, g, ora, **kw):
 @pytest.mark.parametrize("env", [
     {"PGSI_INC_E_V2": "0"},                        # E built by a separate pass over D
     {"PGSI_INC_FUSE_E": "1"},                      # E built inside the closure scan
+    {"PGSI_INC_CLOSURE": "0"},                     # level-synchronous closure (grid barrier per level)
+    {"PGSI_INC_CLO_CAP": "4"},                     # block-local closure: frontier / staging overflow
+    {"PGSI_INC_CLO_CAP": "1", "PGSI_INC_GRID_MUL": "1"},   # every child overflows; tiny grids
+    {"PGSI_INC_CLOSURE": "0", "PGSI_INC_BLK": "0"},
     {"PGSI_INC_BLK": "0"},                         # no block-0 thin-frontier mode
     {"PGSI_INC_BLK": "1"},                         # grid <-> block transitions at every level
     {"PGSI_INC_BLK": "4096"},                      # block mode for wide frontiers too
