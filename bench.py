@@ -26,6 +26,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import re
 import statistics
 import sys
 import threading
@@ -64,19 +65,32 @@ THROTTLE_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_p
                  0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
 
 
+def profile_dir():
+    """The latest round's committed ncu artefacts (profiles/r<N>/kernel_traffic.json)."""
+    rounds = sorted((d for d in os.listdir(os.path.join(ROOT, "profiles")) if re.fullmatch(r"r\d+", d)),
+                    key=lambda d: int(d[1:]))
+    for d in reversed(rounds):
+        if os.path.exists(os.path.join(ROOT, "profiles", d, "kernel_traffic.json")):
+            return d
+    return None
+
+
 def ncu_traffic(kernel_prefix):
-    """DRAM bytes per launch of a kernel from the committed ncu launch list of this
-    round (profiles/r1/kernel_traffic.json, written by scripts/traffic_json.py from
-    `ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,...` over one bench
-    solve; cold-cache, serialised launches). None if not profiled."""
-    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1", "kernel_traffic.json")
+    """DRAM bytes per launch of a kernel from the committed ncu launch list of the
+    latest profiled round (profiles/r<N>/kernel_traffic.json, written by
+    scripts/traffic_json.py from `ncu --metrics dram__bytes_read.sum,
+    dram__bytes_write.sum,...` over one bench solve; cold-cache, serialised launches).
+    None if not profiled."""
+    d = profile_dir()
+    if d is None:
+        return None, None
     try:
-        data = json.load(open(path))
+        data = json.load(open(os.path.join(ROOT, "profiles", d, "kernel_traffic.json")))
     except (OSError, ValueError):
         return None, None
     for k, v in data.get("kernels", {}).items():
         if k.replace("void ", "").startswith(kernel_prefix):
-            return v["dram_bytes_per_launch"], "profiles/r1/kernel_traffic.json (ncu launch list, per-launch mean)"
+            return v["dram_bytes_per_launch"], f"profiles/{d}/kernel_traffic.json (ncu launch list, per-launch mean)"
     return None, None
 
 
@@ -85,16 +99,18 @@ def ncu_dram_summary(peak):
     config-3 solve: actual DRAM bytes / duration per kernel (cold-cache, serialised
     launches), and the time-weighted aggregates of the valuation kernels and of the
     switch kernels. None if the profile is absent."""
-    path = os.path.join(ROOT, "profiles", "r1", "kernel_traffic.json")
+    d = profile_dir()
+    if d is None:
+        return None
     try:
-        ks = json.load(open(path))["kernels"]
+        ks = json.load(open(os.path.join(ROOT, "profiles", d, "kernel_traffic.json")))["kernels"]
     except (OSError, ValueError, KeyError):
         return None
     groups = {"valuation (k_v1, k_spl_*, k_v2_cpx, k_inc_iter)": ("k_v1", "k_spl_", "void k_spl_", "k_v2_cpx", "k_inc_iter"),
               "odd switch (k_switch<1,*>)": ("void k_switch<1",),
               "even switch (k_switch<0,*>, k_ebuild_even)": ("void k_switch<0", "k_ebuild_even"),
               "bellman-ford round (k_bf_round)": ("void k_bf_round",)}
-    out = {"source": "profiles/r1/kernel_traffic.json", "peak_GBps": peak, "groups": {}}
+    out = {"source": f"profiles/{d}/kernel_traffic.json", "peak_GBps": peak, "groups": {}}
     for name, prefixes in groups.items():
         b = t = 0.0
         for k, v in ks.items():
@@ -180,21 +196,53 @@ def make_game(wl, seed):
     return gi.random_game(wl["n"], wl["d"], wl["lo"], wl["hi"], seed)
 
 
+def host_cpu():
+    """CPU model name and logical CPU count of this host."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return model, os.cpu_count()
+
+
 def oracle_sample(game, iters):
     """Time the plain oracle (as it stands) on the first `iters` valuations of the
-    solve: returns (valuations/s, seconds, iterations done)."""
+    solve, pinned to one host core (sched_setaffinity; restored afterwards):
+    returns (valuations/s, seconds, iterations done, core)."""
     from oracle import Oracle, OracleError
     o = Oracle(game)                       # load/preprocess: not timed (PAPER.md:939-940)
-    t0 = time.perf_counter()
+    old = os.sched_getaffinity(0)
+    core = sorted(old)[0]
+    os.sched_setaffinity(0, {core})
     try:
-        r = o.solve(max_inner=iters)
-        done = r.inner_iters
-    except OracleError as e:
-        if e.name != "EITERCAP":
-            raise
-        done = iters
-    dt = time.perf_counter() - t0
-    return game.n * done / dt, dt, done
+        t0 = time.perf_counter()
+        try:
+            r = o.solve(max_inner=iters)
+            done = r.inner_iters
+        except OracleError as e:
+            if e.name != "EITERCAP":
+                raise
+            done = iters
+        dt = time.perf_counter() - t0
+    finally:
+        os.sched_setaffinity(0, old)
+    return game.n * done / dt, dt, done, core
+
+
+def full_solve_record(workload):
+    """The committed full oracle solve of this workload (profiles/r2/oracle_cpu_baseline.json,
+    scripts/oracle_timing.py: one pinned core of the development host), or None."""
+    try:
+        rec = json.load(open(os.path.join(ROOT, "profiles", "r2", "oracle_cpu_baseline.json")))
+        g = rec["games"][workload]
+        return {"valuations_per_s": g["valuations_per_s"], "solve_s": g["solve_s"], "inner_iters": g["inner_iters"],
+                "host": rec["host"]["model"], "source": "profiles/r2/oracle_cpu_baseline.json (not re-measured here)"}
+    except (OSError, KeyError, ValueError):
+        return None
 
 
 def run_reference(args, wl, rank):
@@ -209,19 +257,22 @@ def run_reference(args, wl, rank):
         oracle_sample(game, iters)
     tot_units, tot_s = 0.0, 0.0
     for _ in range(args.steps):
-        v, dt, done = oracle_sample(game, iters)
+        v, dt, done, core = oracle_sample(game, iters)
         tot_units += game.n * done
         tot_s += dt
     value = tot_units / tot_s
-    sample = (f"first {iters} valuation(s) of Algorithm 1 on the {wl['desc']} game per step "
-              f"(oracle load/preprocess excluded)")
+    model, ncpu = host_cpu()
+    sample = (f"first {iters} valuation(s) of Algorithm 1 on the {wl['desc']} game per step, "
+              f"pinned to core {core} of {ncpu} ({model}); oracle load/preprocess excluded")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * tot_s / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
         "data": "synthetic", "config": {"workload": wl["desc"], "n": game.n, "d": wl.get("d"),
                                         "seed": args.seed, "parallelism": "cpu-1thread"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
+                         "host_cpu": model, "host_logical_cpus": ncpu,
+                         "full_solve": full_solve_record(args.workload)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -335,21 +386,24 @@ def main():
     # ---- per-phase CUDA events (PG_PHASE_TIMING): kernel times for the roofline block.
     # Events around every phase need the host-driven loop, so these are separate solves of
     # the same game right after the timed region (same kernels, same launch sequence).
-    Gp = join(Game.from_game(game, device=local, stream=stream.cuda_stream, device_ptrs=True, phase_timing=True))
-    Gp.solve(out=out)
-    acc = {k: 0.0 for k in acc}
-    torch.cuda.synchronize(dev)
-    ep0 = torch.cuda.Event(enable_timing=True)
-    ep1 = torch.cuda.Event(enable_timing=True)
-    ep0.record(stream)
-    for _ in range(args.steps):
-        r = Gp.solve(out=out)
-        for k in acc:
-            acc[k] += r.stats[k]
-    ep1.record(stream)
-    torch.cuda.synchronize(dev)
-    host_loop_ms = ep0.elapsed_time(ep1) / args.steps
-    Gp.free()
+    host_loop_ms = float("nan")
+    if not args.profile:   # (--profile: the launch list of exactly the timed solves)
+        Gp = join(Game.from_game(game, device=local, stream=stream.cuda_stream, device_ptrs=True,
+                                 phase_timing=True))
+        Gp.solve(out=out)
+        acc = {k: 0.0 for k in acc}
+        torch.cuda.synchronize(dev)
+        ep0 = torch.cuda.Event(enable_timing=True)
+        ep1 = torch.cuda.Event(enable_timing=True)
+        ep0.record(stream)
+        for _ in range(args.steps):
+            r = Gp.solve(out=out)
+            for k in acc:
+                acc[k] += r.stats[k]
+        ep1.record(stream)
+        torch.cuda.synchronize(dev)
+        host_loop_ms = ep0.elapsed_time(ep1) / args.steps
+        Gp.free()
 
     # ---- roofline of the dominant kernel (phase with the largest event time)
     peak, peak_src = measured_peak_gbs()
@@ -488,10 +542,14 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline and not args.profile:
         from oracle import build_oracle
         build_oracle()
-        v, dt, done = oracle_sample(game, wl["cpu_iters"])
+        v, dt, done, core = oracle_sample(game, wl["cpu_iters"])
+        model, ncpu = host_cpu()
         cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-               "sample": f"first {done} valuations of Algorithm 1 on this game ({dt:.1f} s, "
-                         f"1 host thread, oracle load excluded)"}
+               "sample": f"first {done} valuations of Algorithm 1 on this game ({dt:.1f} s, one thread pinned "
+                         f"to core {core} of {ncpu}; oracle load excluded). The first valuations from "
+                         f"sigma_init are the cheapest of a solve: full_solve is the whole solve",
+               "host_cpu": model, "host_logical_cpus": ncpu,
+               "full_solve": full_solve_record(args.workload)}
 
     if rank == 0:
         ws_bytes = (G.n_internal + 1) * (32 + 8 + 4 + 1 + 1) + 8 * int(game.m)

@@ -1,9 +1,9 @@
 """Turn a gpurun_out/prof/ directory written by scripts/profile_round.sh into the
-committed profiles/r1/ artefacts: launch lists + per-kernel summary, per-kernel
+committed profiles/<round>/ artefacts: launch lists + per-kernel summary, per-kernel
 DRAM traffic JSON (bench.py's roofline.traffic / hbm_actual), the --set full
 detail digests, k_inc_iter's stall lines and the phase trace.
 
-    python scripts/postprocess_profiles.py [gpurun_out/prof] [profiles/r1] [bench.json]
+    python scripts/postprocess_profiles.py [gpurun_out/prof] [profiles/r2] [bench.json]
 """
 import csv
 import io
@@ -16,7 +16,8 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 src = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "gpurun_out", "prof")
-dst = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "profiles", "r1")
+dst = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "profiles", "r2")
+rnd = os.path.basename(os.path.normpath(dst))
 bench_line = sys.argv[3] if len(sys.argv) > 3 else None
 S = os.path.join(ROOT, "scripts")
 
@@ -39,7 +40,7 @@ a = json.load(open("/tmp/_t1.json"))
 if os.path.exists(os.path.join(src, "launches_bf.csv")):
     run(f"python {S}/traffic_json.py {src}/launches_bf.csv /tmp/_t2.json")
     a["kernels"].update(json.load(open("/tmp/_t2.json"))["kernels"])
-a["source"] = ("profiles/r1/launches_cfg3.csv (one config-3 solve) + profiles/r1/launches_bf_cfg3.csv "
+a["source"] = (f"profiles/{rnd}/launches_cfg3.csv (one config-3 solve) + profiles/{rnd}/launches_bf_cfg3.csv "
                "(200 Bellman-Ford rounds, config 3)")
 json.dump(a, open(os.path.join(dst, "kernel_traffic.json"), "w"), indent=1)
 
@@ -83,14 +84,16 @@ if len(rows) > 3:
               for d in sorted(data, key=lambda x: -x[1])[:15]]
     open(os.path.join(dst, "ncu_k_inc_iter_stall_lines.txt"), "w").write("\n".join(lines) + "\n")
 
-# phase trace (second solve)
-tr = os.path.join(src, "trace.log")
+# phase trace (scripts/trace_solve.py: the second, traced solve)
+tr = os.path.join(src, "inc_phase_trace.txt")
 if os.path.exists(tr):
-    sel = [l for l in open(tr).read().splitlines() if l.startswith("[pgsi]")]
+    txt = open(tr).read()
+    txt = txt.split("---- traced solve", 1)[-1]
+    sel = [l for l in txt.splitlines() if l.startswith("[pgsi]")]
     open(os.path.join(dst, "inc_phase_trace.txt"), "w").write(
-        "# PGSI_TRACE=2 over one config-3 solve (bench.py --profile, second solve): per valuation\n"
-        "# (inc=1: incremental step, one per launch under tracing) the k_inc_iter phase times from %globaltimer (us)\n"
-        + "\n".join(sel[len(sel) // 2:]) + "\n")
+        "# PGSI_TRACE=2 over one config-3 solve (scripts/trace_solve.py, second solve; host-driven loop, one\n"
+        "# incremental step per launch under tracing): per valuation the k_inc_iter phase times from %globaltimer (us)\n"
+        + "\n".join(sel) + "\n")
 
 # the bench line, with hbm_actual recomputed from the traffic JSON just written
 if bench_line:
