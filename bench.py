@@ -347,7 +347,7 @@ def main():
                             "n_even", "n_inc", "gpu_launches", "inner_iters", "outer_passes",
                             "full_compares", "v1_rounds", "v2_split_valuations", "inc_valuations",
                             "dirty_vertices", "ms_bfs", "n_bfs", "bytes_bfs", "bfs_valuations",
-                            "prefix_gathers", "device_loop_solves", "small_solves")}
+                            "prefix_gathers", "device_loop_solves", "small_solves", "cluster_solves")}
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     barrier()
@@ -569,7 +569,9 @@ def main():
                        "mean_dirty_fraction": (acc["dirty_vertices"] / max(acc["inc_valuations"], 1)) / G.n_internal,
                        "loop": ("device: one CUDA graph launch per solve (conditional WHILE/SWITCH nodes)"
                                 if timed_stats["device_loop_solves"] else
-                                "single-block whole-solve kernel" if timed_stats["small_solves"] else "host-driven"),
+                                "single-block whole-solve kernel" if timed_stats["small_solves"] else
+                                "whole-solve kernel on one thread-block cluster (DSMEM)"
+                                if timed_stats["cluster_solves"] else "host-driven"),
                        "host_loop_ms_per_solve": host_loop_ms,
                        "parallelism": ("single GPU" if world == 1 else
                                        f"strong: one game, switch steps sharded over {world} GPUs, valuation "

@@ -179,6 +179,9 @@ typedef struct {
                                 (4 B per Odd vertex), and R = 4·dp bytes per row gathered
                                 (candidates, the vertex's previous row) or written (finite
                                 new rows; ⊤ is encoded in the row)                          */
+    int64_t cluster_solves;  /* pg_solve calls run entirely by one thread-block cluster of up to
+                                16 CTAs (k_solve_cluster: the state of k_solve_small sharded
+                                over the CTAs' distributed shared memory)                 */
 } pg_stats;
 
 /* pg_load: validate, canonicalise and preprocess a game, copy it to the GPU.

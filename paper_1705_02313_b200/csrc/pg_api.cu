@@ -78,6 +78,13 @@ struct pg_game_s {
     int64_t *h_x = nullptr;           // pinned scratch (exchange counts, total |S|)
     // whole-solve single-block path for small games (pg_small.cu)
     int64_t small_max = INT64_MAX;    // n' + 1 up to this (PGSI_SMALL_MAX; 0 disables)
+    int64_t cluster_max = INT64_MAX;  // whole solve on a thread-block cluster up to this n' + 1 (PGSI_CLUSTER_MAX)
+    // PGSI_CLUSTER: 0 = never; 1 (default) = when the game fits a cluster and the last
+    // solve on this handle was iteration-bound (inner_iters * 4 >= n': the multi-kernel
+    // path pays tens of µs per iteration whatever the size, the cluster kernel pays per
+    // vertex; scripts/cluster_probe.py); 2 = whenever the game fits
+    int cluster_mode = 1;
+    int64_t last_inner = 0;
     int smem_optin = 0;               // max dynamic shared memory per block (bytes)
     // Bellman-Ford arm (PG_BELLMAN_FORD): double-buffered key rows (⊤ = all INT_MAX)
     int32_t *bf_row[2] = {nullptr, nullptr};
@@ -1112,6 +1119,8 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     G.inc_grid_cap = h->lc.coop_inc;
     G.inc_grid_mul = getenv("PGSI_INC_GRID_MUL") ? atoi(getenv("PGSI_INC_GRID_MUL")) : 16;
     if (getenv("PGSI_SMALL_MAX")) h->small_max = atoll(getenv("PGSI_SMALL_MAX"));
+    if (getenv("PGSI_CLUSTER_MAX")) h->cluster_max = atoll(getenv("PGSI_CLUSTER_MAX"));
+    if (getenv("PGSI_CLUSTER")) h->cluster_mode = atoi(getenv("PGSI_CLUSTER"));
     if (getenv("PGSI_DEVICE_LOOP")) h->device_loop = atoi(getenv("PGSI_DEVICE_LOOP"));
     if (cudaDeviceGetAttribute(&h->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device) != cudaSuccess)
         h->smem_optin = 48 * 1024;
@@ -1423,17 +1432,47 @@ pg_status pg_solve(pg_game h, uint8_t *winner, int32_t *sigma, int32_t *tau, int
                 rc = PG_EINADMISSIBLE;
             }
         }
+        // too large for one block: the whole solve on one thread-block cluster (up to 16
+        // SMs' shared memory) when the state fits there
+        const bool cluster_want = h->cluster_mode == 2 || (h->cluster_mode == 1 && h->last_inner * 4 >= h->G.n_int);
+        const int cluster_C = (!small && cluster_want && h->G.n_int + 1 <= h->cluster_max && !dist_active(h) &&
+                               !check && !h->trace &&
+                               !(h->flags & (PG_BELLMAN_FORD | PG_TRACE | PG_PHASE_TIMING | PG_BFS)))
+                                  ? cluster_size_for(h->G.n_int, h->G.dp, (size_t)h->smem_optin - 1024)
+                                  : 0;
+        if (cluster_C) {
+            {
+                PhaseScope ps(h, PH_OTHER);
+                CK(h, launch_solve_cluster(h->G, cluster_C, (h->flags & PG_SI_RESET) != 0, h->max_inner,
+                                           h->max_outer, h->stream));
+                h->st.gpu_launches += 1;
+            }
+            if ((rc = readback(h))) return rc;
+            inner = (int64_t)h->h_ctl->sm_inner;
+            outer = (int64_t)h->h_ctl->sm_outer;
+            h->st.v1_rounds += (int64_t)h->h_ctl->v1_rounds;
+            h->st.odd_switches += (int64_t)h->h_ctl->odd_switches;
+            h->st.even_switches += (int64_t)h->h_ctl->even_switches;
+            h->st.cluster_solves++;
+            h->have_state = false;
+            h->c_valid = false;
+            if (h->h_ctl->sm_status == 1) {
+                set_err(h->max_outer > 0 && outer >= h->max_outer ? "outer pass cap reached" : "inner iteration cap reached");
+                rc = PG_EITERCAP;
+            }
+        }
+        const bool on_chip = small || cluster_C;
         // Algorithm 1 on the device (pg_loop.cu) unless a host-side feature is on:
         // per-phase CUDA events, the trace, sharding, the BFS valuation, the
         // Bellman-Ford arm, or odd-cycle checks (cycle-dominant priorities)
-        const bool graph = !small && (h->device_loop == 2 || (h->device_loop == 1 && h->solves > 0)) && !check &&
+        const bool graph = !on_chip && (h->device_loop == 2 || (h->device_loop == 1 && h->solves > 0)) && !check &&
                            !dist_active(h) && !h->trace &&
                            !(h->flags & (PG_PHASE_TIMING | PG_TRACE | PG_BFS | PG_BELLMAN_FORD));
         if (graph) {
             PhaseScope ps(h, PH_OTHER);
             rc = solve_graph(h, &inner, &outer);
         }
-        for (; !small && !graph;) {                          // Algorithm 1, outer repeat
+        for (; !on_chip && !graph;) {                        // Algorithm 1, outer repeat
             if (h->max_outer > 0 && outer >= h->max_outer) {
                 set_err("outer pass cap reached");
                 rc = PG_EITERCAP;
@@ -1457,6 +1496,7 @@ pg_status pg_solve(pg_game h, uint8_t *winner, int32_t *sigma, int32_t *tau, int
     h->st.inner_iters = inner;
     h->st.outer_passes = outer;
     h->solves++;
+    h->last_inner = inner;
     if (rc) { timing_collect(h); if (stats) *stats = h->st; return rc; }
     const int64_t n = h->n;
     std::vector<OutBuf> outs = {{winner, nullptr, (size_t)n},

@@ -29,6 +29,7 @@
 // Per outer pass, All_Even (greedy all-switches, sink candidate last). Results and
 // iteration counts are identical to the multi-kernel path; the GPU tests check both
 // against the oracle.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -223,6 +224,215 @@ cudaError_t launch_solve_small(const DevGame &g, bool check, bool reset, int64_t
     }
     k_solve_small<<<1, kSmallThreads, L.total, s>>>(g, L, check ? 1 : 0, reset ? 1 : 0, max_inner, max_outer);
     return cudaGetLastError();
+}
+
+// --------------------------------------------------------------------------
+// The same whole-solve loop on a THREAD-BLOCK CLUSTER (up to 16 CTAs, one per SM,
+// distributed shared memory): games whose state does not fit one SM's 227 KB
+// (n' · (8·dp + 9) bytes) but fits C of them. CTA r of the cluster owns the
+// contiguous vertex shard [r·S, (r+1)·S) of rows, J and ⊤ flags in its shared
+// memory; a vertex w's data lives in CTA w / S and is read through DSMEM
+// (cluster.map_shared_rank: ~215 cycles on B200-class parts). Every __syncthreads of
+// the single-block kernel becomes a cluster barrier (barrier.cluster, ~380 cycles),
+// and every count a cluster-wide sum. No check mode here (the host takes the
+// multi-kernel path for PG_CHECK_INVARIANTS / PG_NO_PREPROCESS).
+// --------------------------------------------------------------------------
+namespace cg = cooperative_groups;
+
+struct ClusterLayout {   // offsets inside each CTA's dynamic shared memory; S = vertices per CTA
+    int32_t S, C;
+    size_t rows[2], J[2], top, total;
+};
+
+static ClusterLayout cluster_layout(int64_t n1, int dp, int C) {
+    ClusterLayout L{};
+    L.C = C;
+    L.S = (int32_t)((n1 + C - 1) / C);
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 15) & ~size_t(15); return o; };
+    for (int b = 0; b < 2; b++) L.rows[b] = take((size_t)L.S * dp * 4);
+    for (int b = 0; b < 2; b++) L.J[b] = take((size_t)L.S * 4);
+    L.top = take((size_t)L.S);
+    L.total = off;
+    return L;
+}
+
+// smallest cluster size (2..16) whose per-CTA state fits smem_per_cta; 0 if none
+int cluster_size_for(int64_t n_int, int dp, size_t smem_per_cta) {
+    for (int C = 2; C <= 16; C *= 2)
+        if (cluster_layout(n_int + 1, dp, C).total <= smem_per_cta) return C;
+    return 0;
+}
+
+// cluster-wide sum of one value per thread (all threads of all CTAs call it)
+__device__ __forceinline__ int cl_sum(cg::cluster_group &cl, int *s_part, int &parity, int x) {
+    __shared__ int s_acc;
+    if (threadIdx.x == 0) s_acc = 0;
+    __syncthreads();
+    if (x) atomicAdd(&s_acc, x);
+    __syncthreads();
+    if (threadIdx.x == 0) s_part[parity] = s_acc;
+    cl.sync();
+    int tot = 0;
+    const int C = (int)cl.num_blocks();
+    for (int q = 0; q < C; q++) tot += *cl.map_shared_rank(s_part + parity, q);
+    parity ^= 1;
+    return tot;
+}
+
+__global__ void __launch_bounds__(kSmallThreads) k_solve_cluster(DevGame g, ClusterLayout L, int reset,
+                                                                 int64_t max_inner, int64_t max_outer) {
+    extern __shared__ int4 smem4[];
+    __shared__ int s_part[2];
+    cg::cluster_group cl = cg::this_cluster();
+    const int r = (int)cl.block_rank();
+    char *base = reinterpret_cast<char *>(smem4);
+    int32_t *const rowsL[2] = {reinterpret_cast<int32_t *>(base + L.rows[0]), reinterpret_cast<int32_t *>(base + L.rows[1])};
+    int32_t *const JL[2] = {reinterpret_cast<int32_t *>(base + L.J[0]), reinterpret_cast<int32_t *>(base + L.J[1])};
+    uint8_t *const topL = reinterpret_cast<uint8_t *>(base + L.top);
+    const int32_t N = (int32_t)g.n_int, SINK = N, S = L.S;
+    const int dp = g.dp;
+    const int t = threadIdx.x, T = blockDim.x;
+    const int32_t lo = r * S, hi = min(lo + S, N + 1);   // this CTA's vertices (the sink is the last)
+    // the CTA-local pointer of vertex w's entry in a per-vertex array at local offset `a`
+    auto rowp = [&](int b, int32_t w) -> const int32_t * {
+        const int o = w / S;
+        return cl.map_shared_rank(rowsL[b], o) + (w - o * S);
+    };
+    auto jp = [&](int b, int32_t w) -> const int32_t * {
+        const int o = w / S;
+        return cl.map_shared_rank(JL[b], o) + (w - o * S);
+    };
+    auto topv = [&](int32_t w) -> bool {
+        const int o = w / S;
+        return *(cl.map_shared_rank(topL, o) + (w - o * S)) != 0;
+    };
+    // a ⊏ b on (row, ⊤) pairs of buffer b_; the sink is the finite zero row
+    auto less = [&](int b_, int32_t a, int32_t b) -> bool {
+        const bool ta = a != SINK && topv(a), tb = b != SINK && topv(b);
+        if (ta) return false;
+        if (tb) return true;
+        const int32_t *ra = a == SINK ? nullptr : rowp(b_, a), *rb = b == SINK ? nullptr : rowp(b_, b);
+        for (int i = dp - 1; i >= 0; i--) {
+            const int32_t x = ra ? ra[(int64_t)i * S] : 0, y = rb ? rb[(int64_t)i * S] : 0;
+            if (x != y) return x < y;
+        }
+        return false;
+    };
+    int parity = 0;
+    int64_t inner = 0, outer = 0, rounds = 0, odd_sw = 0, even_sw = 0;
+    int status = 0;
+    int cur = 0;
+    for (;;) {                                                        // Algorithm 1, outer repeat
+        if (max_outer > 0 && outer >= max_outer) { status = 1; break; }
+        if (reset && outer > 0) {                                     // SI-Reset: τ := τ_init
+            for (int32_t v = max(lo, (int32_t)g.n_even) + t; v < min(hi, N); v += T) g.succ[v] = g.col[g.rp[v]];
+            cl.sync();
+        }
+        bool stop = false;
+        for (;;) {                                                    // inner repeat
+            if (max_inner > 0 && inner >= max_inner) { status = 1; stop = true; break; }
+            for (int32_t v = lo + t; v < hi; v += T) {                // round 0 = (succ, e_pri)
+                const int p = v < N ? g.pidx[v] : -1;
+                for (int i = 0; i < dp; i++) rowsL[0][(int64_t)i * S + (v - lo)] = i == p ? (g.oddp[p] ? -1 : 1) : 0;
+                JL[0][v - lo] = v < N ? g.succ[v] : SINK;
+            }
+            cl.sync();
+            int c = 0;
+            for (;;) {                                                // Wyllie rounds
+                int newly = 0;
+                for (int32_t v = lo + t; v < min(hi, N); v += T) {
+                    const int32_t w = JL[c][v - lo];
+                    int32_t *rn = rowsL[c ^ 1] + (v - lo);
+                    const int32_t *rv = rowsL[c] + (v - lo);
+                    if (w == SINK) {
+                        for (int i = 0; i < dp; i++) rn[(int64_t)i * S] = rv[(int64_t)i * S];
+                        JL[c ^ 1][v - lo] = SINK;
+                    } else {
+                        const int32_t *rw = rowp(c, w);
+                        for (int i = 0; i < dp; i++) rn[(int64_t)i * S] = rv[(int64_t)i * S] + rw[(int64_t)i * S];
+                        const int32_t jw = *jp(c, w);
+                        JL[c ^ 1][v - lo] = jw;
+                        newly += jw == SINK;
+                    }
+                }
+                if (lo <= N && N < hi && t == 0) JL[c ^ 1][N - lo] = SINK;
+                rounds++;
+                c ^= 1;
+                if (cl_sum(cl, s_part, parity, newly) == 0) break;   // (its cluster barrier publishes the round)
+            }
+            cur = c;
+            for (int32_t v = lo + t; v < min(hi, N); v += T) topL[v - lo] = JL[cur][v - lo] != SINK;
+            cl.sync();
+            inner++;
+            int sw = 0;                                               // All_Odd, in place
+            for (int32_t v = max(lo, (int32_t)g.n_even) + t; v < min(hi, N); v += T) {
+                const uint32_t e0 = g.rp[v], e1 = g.rp[v + 1];
+                int32_t best = g.col[e0];
+                for (uint32_t e = e0 + 1; e < e1; e++) {
+                    const int32_t u = g.col[e];
+                    if (less(cur, u, best)) best = u;
+                }
+                const int32_t cu = g.succ[v];
+                if (best != cu && less(cur, best, cu)) { g.succ[v] = best; sw++; }
+            }
+            const int nsw = cl_sum(cl, s_part, parity, sw);
+            odd_sw += nsw;
+            if (nsw == 0) break;
+        }
+        if (stop) break;
+        outer++;
+        int sw = 0;                                                   // All_Even (sink candidate last)
+        for (int32_t v = lo + t; v < min(hi, (int32_t)g.n_even); v += T) {
+            const uint32_t e0 = g.rp[v], e1 = g.rp[v + 1];
+            int32_t best = g.col[e0];
+            for (uint32_t e = e0 + 1; e < e1; e++) {
+                const int32_t u = g.col[e];
+                if (less(cur, best, u)) best = u;
+            }
+            if (less(cur, best, SINK)) best = SINK;
+            const int32_t cu = g.succ[v];
+            if (best != cu && less(cur, cu, best)) { g.succ[v] = best; sw++; }
+        }
+        const int nsw = cl_sum(cl, s_part, parity, sw);
+        even_sw += nsw;
+        if (nsw == 0) break;
+    }
+    for (int32_t v = lo + t; v < min(hi, N); v += T) g.top[v] = topL[v - lo];
+    if (r == 0 && t == 0) {
+        Ctl *ctl = g.ctl;
+        ctl->sm_inner = (unsigned long long)inner;
+        ctl->sm_outer = (unsigned long long)outer;
+        ctl->sm_status = (unsigned long long)status;
+        ctl->v1_rounds = (unsigned long long)rounds;
+        ctl->odd_switches = (unsigned long long)odd_sw;
+        ctl->even_switches = (unsigned long long)even_sw;
+    }
+    cl.sync();   // no CTA leaves while another may still read its shared memory
+}
+
+cudaError_t launch_solve_cluster(const DevGame &g, int C, bool reset, int64_t max_inner, int64_t max_outer,
+                                 cudaStream_t s) {
+    const ClusterLayout L = cluster_layout(g.n_int + 1, g.dp, C);
+    cudaError_t e = cudaFuncSetAttribute(k_solve_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
+    if (e) return e;
+    if (C > 8) {
+        e = cudaFuncSetAttribute(k_solve_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e) return e;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)C);
+    cfg.blockDim = dim3(kSmallThreads);
+    cfg.dynamicSmemBytes = L.total;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_solve_cluster, g, L, reset ? 1 : 0, max_inner, max_outer);
 }
 
 }  // namespace pgsi

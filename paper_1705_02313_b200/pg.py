@@ -68,7 +68,7 @@ class Stats(C.Structure):
         ("dist_exchanges", C.c_int64), ("dist_bytes", C.c_int64), ("ms_dist", C.c_double),
         ("prefix_gathers", C.c_int64), ("small_solves", C.c_int64),
         ("bf_rounds", C.c_int64), ("ms_bf", C.c_double), ("n_bf", C.c_int64),
-        ("device_loop_solves", C.c_int64), ("bytes_bf", C.c_double)]
+        ("device_loop_solves", C.c_int64), ("bytes_bf", C.c_double), ("cluster_solves", C.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -9,9 +9,10 @@ import numpy as np
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 n, d = int(sys.argv[1]), int(sys.argv[2])
-if len(sys.argv) > 3 and sys.argv[3] == "multikernel":
+if len(sys.argv) > 3 and sys.argv[3] in ("multikernel", "cluster"):
     os.environ["PGSI_SMALL_MAX"] = "0"
     os.environ["PGSI_HOST_LOAD_MAX"] = "0"
+    os.environ["PGSI_CLUSTER"] = "0" if sys.argv[3] == "multikernel" else "2"
 import pg_inputs as gi  # noqa: E402
 from oracle import Oracle  # noqa: E402
 from paper_1705_02313_b200 import Game  # noqa: E402

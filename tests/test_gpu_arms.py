@@ -20,6 +20,7 @@ def solve_path(request, monkeypatch):
     with that path disabled (PGSI_SMALL_MAX=0), so both paths meet the oracle."""
     if request.param == "multikernel":
         monkeypatch.setenv("PGSI_SMALL_MAX", "0")
+        monkeypatch.setenv("PGSI_CLUSTER", "0")
     return request.param
 
 

@@ -35,6 +35,7 @@ def same(r, ora, n):
 @pytest.mark.parametrize("seed", range(10))
 def test_device_loop_matches_oracle_and_host_loop(pg, monkeypatch, seed):
     monkeypatch.setenv("PGSI_SMALL_MAX", "0")
+    monkeypatch.setenv("PGSI_CLUSTER", "0")
     monkeypatch.setenv("PGSI_DEVICE_LOOP", "2")
     rng = np.random.default_rng(700 + seed)
     n = int(rng.integers(20_000, 300_000))
@@ -55,6 +56,7 @@ def test_device_loop_matches_oracle_and_host_loop(pg, monkeypatch, seed):
 @pytest.mark.parametrize("fam", ["ladder", "elevator", "deep", "oddchain", "stair"])
 def test_device_loop_structured(pg, monkeypatch, fam):
     monkeypatch.setenv("PGSI_SMALL_MAX", "0")
+    monkeypatch.setenv("PGSI_CLUSTER", "0")
     monkeypatch.setenv("PGSI_DEVICE_LOOP", "2")
     g = {"ladder": lambda: gi.ladder(60_000, 2), "elevator": lambda: gi.elevator(12, 10, 1),
          "deep": lambda: gi.f_deep(50_000), "oddchain": lambda: gi.f_oddchain(3_000),
@@ -67,6 +69,7 @@ def test_device_loop_structured(pg, monkeypatch, fam):
 
 def test_device_loop_si_reset_and_caps(pg, monkeypatch):
     monkeypatch.setenv("PGSI_SMALL_MAX", "0")
+    monkeypatch.setenv("PGSI_CLUSTER", "0")
     monkeypatch.setenv("PGSI_DEVICE_LOOP", "2")
     g = gi.random_game(80_000, 12, 2, 5, 4)
     ora = Oracle(g).solve(mode="si_reset")
@@ -90,6 +93,7 @@ def test_device_loop_default_policy(pg, monkeypatch):
     """Default (PGSI_DEVICE_LOOP unset): the first pg_solve of a handle runs the
     host-driven loop, later ones the graph; all equal."""
     monkeypatch.setenv("PGSI_SMALL_MAX", "0")
+    monkeypatch.setenv("PGSI_CLUSTER", "0")
     monkeypatch.delenv("PGSI_DEVICE_LOOP", raising=False)
     g = gi.random_game(90_000, 16, 2, 5, 6)
     ora = Oracle(g).solve()
@@ -105,6 +109,7 @@ def test_device_loop_splitter_growth(pg, monkeypatch):
     buffers hold. The graph ends with LS_HOST_SPLITTERS; the host grows the buffers,
     rebuilds the graph and resumes."""
     monkeypatch.setenv("PGSI_SMALL_MAX", "0")
+    monkeypatch.setenv("PGSI_CLUSTER", "0")
     monkeypatch.setenv("PGSI_DEVICE_LOOP", "2")
     L = 100_000
     owner = [0] + [1] * L
@@ -121,6 +126,7 @@ def test_device_loop_epoch_wrap(pg, monkeypatch):
     """Mark epochs started just below 2^32: the graph ends with LS_HOST_EPOCHS, the host
     clears the marks and resumes; results unchanged (host loop too)."""
     monkeypatch.setenv("PGSI_SMALL_MAX", "0")
+    monkeypatch.setenv("PGSI_CLUSTER", "0")
     g = gi.random_game(120_000, 16, 2, 5, 8)
     ora = Oracle(g).solve()
     for start in ("0xffffff00", "0xfffffffa"):

@@ -248,6 +248,7 @@ def test_nccl_dist_init_world1_matches_oracle(pg, seed, monkeypatch):
     oracle. One GPU per rank is an NCCL requirement, so world > 1 needs more GPUs; the
     exchange protocol itself is the one the W = 2..4 tests above exercise."""
     monkeypatch.setenv("PGSI_SMALL_MAX", "0")
+    monkeypatch.setenv("PGSI_CLUSTER", "0")
     g = gi.random_game(60_000 + 20_000 * seed, 8 + 8 * seed, 2, 5, seed)
     ora = Oracle(g).solve()
     nid = pg.dist_unique_id()

@@ -57,6 +57,7 @@ def check(pg, g, ora, **kw):
 ])
 def test_inc_knobs_bitexact(pg, games, monkeypatch, env):
     monkeypatch.setenv("PGSI_SMALL_MAX", "0")
+    monkeypatch.setenv("PGSI_CLUSTER", "0")
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     for g, ora in games:

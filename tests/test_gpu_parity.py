@@ -15,13 +15,18 @@ from oracle import Oracle, OracleError
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(autouse=True, params=["auto", "multikernel"])
+@pytest.fixture(autouse=True, params=["auto", "cluster", "multikernel"])
 def solve_path(request, monkeypatch):
-    """Every test runs twice: with the library's default dispatch (games with
-    n' + 1 <= 8192 solve in the single-block whole-solve kernel, k_solve_small) and
-    with that path disabled (PGSI_SMALL_MAX=0), so both paths meet the oracle."""
-    if request.param == "multikernel":
+    """Every test runs three times: with the library's default dispatch (games whose
+    state fits one SM's shared memory solve in the single-block whole-solve kernel,
+    k_solve_small; larger ones that fit a thread-block cluster in k_solve_cluster),
+    with the single-block path disabled (PGSI_SMALL_MAX=0: the cluster kernel takes
+    every game it fits), and with both disabled (the multi-kernel path), so every
+    path meets the oracle."""
+    if request.param in ("cluster", "multikernel"):
         monkeypatch.setenv("PGSI_SMALL_MAX", "0")
+    if request.param != "auto":
+        monkeypatch.setenv("PGSI_CLUSTER", "2" if request.param == "cluster" else "0")
     return request.param
 
 
@@ -270,7 +275,8 @@ def test_solve_forced_full_compares(pg, pairs, k):
         G = pg.Game.from_game(g, prefix_pairs=pairs, splitter_k=k)
         res = G.solve(want_val=True)
         assert_solve_equal(res, ora, n, G.d)
-        assert res.stats["full_compares"] > 0
+        if res.stats["cluster_solves"] == 0:   # (the cluster kernel keeps full rows: no prefixes)
+            assert res.stats["full_compares"] > 0
 
 
 def test_solve_deep_structured_small_k(pg):
@@ -289,7 +295,7 @@ def test_incremental_matches_full_and_oracle(pg, n, d, seed):
     Gi = pg.Game.from_game(g)
     ri = Gi.solve(want_val=True)
     assert_solve_equal(ri, ora, n, Gi.d)
-    assert ri.stats["inc_valuations"] > 0
+    assert ri.stats["inc_valuations"] > 0 or ri.stats["cluster_solves"] == 1
     Gf = pg.Game.from_game(g, incremental=False)
     rf = Gf.solve(want_val=True)
     assert_solve_equal(rf, ora, n, Gf.d)
@@ -390,6 +396,7 @@ def test_bfs_valuation_matches_pipeline(pg, n, d, seed):
 
 def test_bfs_abort_on_deep_game(pg, monkeypatch):
     monkeypatch.setenv("PGSI_SMALL_MAX", "0")   # the BFS valuation belongs to the multi-kernel path
+    monkeypatch.setenv("PGSI_CLUSTER", "0")
     g = gi.f_deep(5000)
     ora = Oracle(g).solve()
     r = pg.Game.from_game(g, bfs=True).solve(want_val=True)
