@@ -94,6 +94,10 @@ struct pg_game_s {
     unsigned long long *tL[2] = {nullptr, nullptr};
     int32_t *tJ[2] = {nullptr, nullptr};
     unsigned long long *tout = nullptr;       // device h_succ, h_val, n_top
+    // V2 design W (PGSI_V2_DESIGN=W, design comparison only): double-buffered rows / pointers
+    bool v2_wyllie = false;
+    int32_t *w_row[2] = {nullptr, nullptr};
+    int32_t *w_J[2] = {nullptr, nullptr};
     // device-resident Algorithm 1 (pg_loop.cu): the instantiated graph and its capture stream
     cudaGraphExec_t loop_exec = nullptr;
     cudaStream_t cap_stream = nullptr;
@@ -286,7 +290,22 @@ pg_status valuate_dev(pg_game h, bool want_cdom, bool full_rows, bool inc = fals
             CK(h, launch_v1(h->G, h->lc, h->stream));
             h->st.gpu_launches += 1;
         }
-        {
+        if (h->v2_wyllie && !full_rows && h->G.dp <= 32) {   // design W (comparison): rounds from V1's depth
+            const size_t N1 = (size_t)h->G.n_int + 1;
+            for (int b = 0; b < 2; b++)
+                if (!h->w_row[b]) {
+                    CK(h, dalloc(h, &h->w_row[b], N1 * h->G.dp));
+                    CK(h, dalloc(h, &h->w_J[b], N1));
+                }
+            unsigned long long md = 0;
+            CK(h, cudaMemcpyAsync(&md, &h->G.ctl->maxdepth, sizeof(md), cudaMemcpyDeviceToHost, h->stream));
+            CK(h, cudaStreamSynchronize(h->stream));
+            int rounds = 0;
+            while ((1ull << rounds) < md + 1) rounds++;
+            PhaseScope ps(h, PH_V2);
+            CK(h, launch_v2_wyllie(h->G, h->w_row, h->w_J, rounds, h->stream));
+            h->st.gpu_launches += rounds + 2;
+        } else {
             PhaseScope ps(h, PH_V2);
             int launches = 0;
             CK(h, launch_splitters(h->G, h->lc, h->stream, &launches));
@@ -1122,6 +1141,8 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     if (getenv("PGSI_CLUSTER_MAX")) h->cluster_max = atoll(getenv("PGSI_CLUSTER_MAX"));
     if (getenv("PGSI_CLUSTER")) h->cluster_mode = atoi(getenv("PGSI_CLUSTER"));
     if (getenv("PGSI_DEVICE_LOOP")) h->device_loop = atoi(getenv("PGSI_DEVICE_LOOP"));
+    h->v2_wyllie = getenv("PGSI_V2_DESIGN") && (getenv("PGSI_V2_DESIGN")[0] == 'W' || getenv("PGSI_V2_DESIGN")[0] == 'w');
+    if (h->v2_wyllie) h->device_loop = 0;   // the W path reads V1's depth back on the host
     if (cudaDeviceGetAttribute(&h->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device) != cudaSuccess)
         h->smem_optin = 48 * 1024;
     G.inc_e_in_v2 = getenv("PGSI_INC_E_V2") ? atoi(getenv("PGSI_INC_E_V2")) : 1;

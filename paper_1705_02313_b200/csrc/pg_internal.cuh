@@ -219,6 +219,7 @@ cudaError_t launch_import_strategy(const DevGame &g, const int32_t *abi_strategy
 cudaError_t launch_v1(const DevGame &g, const LaunchCfg &lc, cudaStream_t s);
 cudaError_t launch_splitters(const DevGame &g, const LaunchCfg &lc, cudaStream_t s, int *launches);
 cudaError_t launch_v2(const DevGame &g, cudaStream_t s, bool full_rows);
+cudaError_t launch_v2_wyllie(const DevGame &g, int32_t *row[2], int32_t *J[2], int rounds, cudaStream_t s);
 cudaError_t launch_cycle_dom(const DevGame &g, const LaunchCfg &lc, cudaStream_t s);
 cudaError_t launch_switch(const DevGame &g, bool odd, cudaStream_t s);
 cudaError_t launch_inc_iter(const DevGame &g, const LaunchCfg &lc, cudaStream_t s, int64_t nS);

@@ -662,6 +662,88 @@ __global__ void __launch_bounds__(kThreads) k_v2_cpx_multi(DevGame g, int nchunk
 }
 
 // --------------------------------------------------------------------------
+// V2 design W (PGSI_V2_DESIGN=W; for the SURVEY §8(a4) design comparison): Wyllie
+// pointer jumping directly over full d-vector key rows (PAPER.md:613-632 applied to
+// the d-vectors), double-buffered rows and pointers, ⌈log2(max depth + 1)⌉ rounds,
+// then each finite row converted to its compact prefix. O(n'·3R·log depth) bytes
+// against design S's walks to depth-strided splitters; DESIGN.md §4 "V2 designs".
+// --------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_w_init(DevGame g, int32_t *row, int32_t *J) {
+    const int64_t N = g.n_int;
+    const int dp = g.dp, q4 = (dp + 3) / 4;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < (N + 1) * q4;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = t / q4;
+        const int q = (int)(t - v * q4);
+        bool fin = false;
+        int p = -1;
+        if (v < N) {
+            fin = (uint32_t)__ldcg(g.jl + v) == (uint32_t)N;
+            p = g.pidx[v];
+        }
+        int32_t k[4];
+#pragma unroll
+        for (int c = 0; c < 4; c++) k[c] = (fin && 4 * q + c == p) ? (g.oddp[p] ? -1 : 1) : 0;
+        if (dp >= 4) *reinterpret_cast<int4 *>(row + v * dp + 4 * q) = make_int4(k[0], k[1], k[2], k[3]);
+        else for (int c = 0; c < dp; c++) row[v * dp + c] = k[c];
+        if (q == 0) J[v] = (v < N && fin) ? __ldg(g.succ + v) : (int32_t)N;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_w_round(int64_t N1, int dp, const int32_t *row, const int32_t *J,
+                                                       int32_t *row2, int32_t *J2, int32_t sink) {
+    const int q4 = (dp + 3) / 4;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < N1 * q4; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t v = t / q4;
+        const int q = (int)(t - v * q4);
+        const int32_t w = __ldg(J + v);
+        if (dp >= 4) {
+            int4 a = __ldg(reinterpret_cast<const int4 *>(row + v * dp + 4 * q));
+            if (w != sink) {
+                const int4 b = __ldg(reinterpret_cast<const int4 *>(row + (int64_t)w * dp + 4 * q));
+                a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+            }
+            *reinterpret_cast<int4 *>(row2 + v * dp + 4 * q) = a;
+        } else {
+            for (int c = 0; c < dp; c++) row2[v * dp + c] = row[v * dp + c] + (w != sink ? row[(int64_t)w * dp + c] : 0);
+        }
+        if (q == 0) J2[v] = w == sink ? sink : __ldg(J + w);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_w_cpx(DevGame g, const int32_t *rows) {
+    const int64_t N = g.n_int;
+    const int dp = g.dp, maxp = g.cpx_pairs;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < N; v += (int64_t)gridDim.x * blockDim.x) {
+        const bool fin = (uint32_t)__ldcg(g.jl + v) == (uint32_t)N;
+        g.top[v] = fin ? 0 : 1;
+        if (!fin) {
+            put_cpx(g, v, make_uint4(1u, 0, 0, 0), make_uint4(0, 0, 0, 0));
+            continue;
+        }
+        const int32_t *row = rows + v * dp;
+        uint32_t w[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        int np = 0;
+        bool trunc = false;
+        for (int col = dp - 1; col >= 0 && !trunc; col--) {
+            const int32_t key = row[col];
+            if (key == 0) continue;
+            if (np >= maxp) { trunc = true; break; }
+            uint32_t mag = (uint32_t)(key < 0 ? -key : key);
+            const bool cap = mag >= kCap;
+            if (cap) mag = kCap;
+            const int32_t en = (int32_t)(((uint32_t)col << 23) + mag);
+#pragma unroll
+            for (int k = 0; k < 7; k++) if (k == np) w[1 + k] = (uint32_t)(key < 0 ? -en : en);
+            np++;
+            if (cap) trunc = true;
+        }
+        w[0] = ((uint32_t)np << 2) | (trunc ? 2u : 0u);
+        put_cpx(g, v, make_uint4(w[0], w[1], w[2], w[3]), make_uint4(w[4], w[5], w[6], w[7]));
+    }
+}
+
+// --------------------------------------------------------------------------
 // Splitter path (only when the deepest finite play has depth >= K).
 // --------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads) k_spl_mark(DevGame g) {
@@ -2141,6 +2223,19 @@ cudaError_t launch_v2(const DevGame &g, cudaStream_t s, bool full_rows) {
 #define WALK(G) k_v2_rows<G><<<grid, kThreads, 0, s>>>(g, nchunk)
     DISPATCH_G(g.dp, WALK);
 #undef WALK
+    return cudaGetLastError();
+}
+
+// design W: init, `rounds` Wyllie rounds, compact prefixes; returns the final buffer
+cudaError_t launch_v2_wyllie(const DevGame &g, int32_t *row[2], int32_t *J[2], int rounds, cudaStream_t s) {
+    const int q4 = (g.dp + 3) / 4;
+    const int64_t N1 = g.n_int + 1;
+    k_w_init<<<grid_for(N1 * q4, kThreads, 32), kThreads, 0, s>>>(g, row[0], J[0]);
+    int c = 0;
+    for (int r = 0; r < rounds; r++, c ^= 1)
+        k_w_round<<<grid_for(N1 * q4, kThreads, 32), kThreads, 0, s>>>(N1, g.dp, row[c], J[c], row[c ^ 1], J[c ^ 1],
+                                                                     (int32_t)g.n_int);
+    k_w_cpx<<<grid_for(g.n_int, kThreads, 16), kThreads, 0, s>>>(g, row[c]);
     return cudaGetLastError();
 }
 
