@@ -532,6 +532,14 @@ pg_status valuate_and_switch(pg_game h, bool odd, bool want_cdom, bool do_switch
         }
         rc = readback(h);
         if (rc) return rc;
+        if (inc && h->h_ctl->split) {   // a big step: V2 / E / All_Odd continue at full occupancy
+            {
+                PhaseScope ps(h, PH_INC);
+                CK(h, launch_inc_split(h->G, h->stream));
+                h->st.gpu_launches += 5;
+            }
+            if ((rc = readback(h))) return rc;
+        }
         if (h->h_ctl->inc_overflow) {   // closure too deep/large or walk too long: redo that step in full
             if (h->h_ctl->steps_done) {  // the steps before it stand
                 done_inc = (int64_t)h->h_ctl->steps_done;
@@ -1151,6 +1159,7 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     G.inc_blk_frontier = getenv("PGSI_INC_BLK") ? atoi(getenv("PGSI_INC_BLK")) : 256;
     G.inc_closure = getenv("PGSI_INC_CLOSURE") ? atoi(getenv("PGSI_INC_CLOSURE")) : 1;
     G.inc_clo_cap = getenv("PGSI_INC_CLO_CAP") ? std::max(1, atoi(getenv("PGSI_INC_CLO_CAP"))) : 1 << 30;
+    G.inc_split_min = getenv("PGSI_INC_SPLIT") ? atoll(getenv("PGSI_INC_SPLIT")) : 131072;
     G.lvlog = nullptr;
     if (trace_levels) {
         CKL(dalloc(h, &G.lvlog, 8192));

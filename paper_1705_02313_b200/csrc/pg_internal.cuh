@@ -66,6 +66,9 @@ struct Ctl {
     unsigned long long nE_sum;      // ... |E| summed over its steps
     unsigned long long cpx_gathers; // switch steps: 32 B prefix gathers after an undecided key compare
     unsigned long long nDl;         // incremental step: D-list length (block-local closure appends)
+    unsigned long long split;       // k_inc_iter stopped after V1 on D: the caller runs launch_inc_split
+    unsigned long long split_nd, split_ep, split_step;
+    unsigned int split_odd_s, split_pad;
     // ---- not reset per valuation ----
     unsigned long long bad_index;   // ULLONG_MAX = none, else min invalid ABI index
     unsigned long long nhard;       // vertices deferred to the hard (full-compare) pass
@@ -169,6 +172,7 @@ struct DevGame {
     int32_t inc_blk_frontier; // closure levels with at most this many frontier vertices run in block 0
     int32_t inc_closure;      // 1 = block-local closure phases (closure_block), 0 = level-synchronous BFS
     int32_t inc_clo_cap;      // closure_block frontier capacity in use (<= kCloCap; testing shrinks it)
+    int64_t inc_split_min;    // |D| from which a step continues in launch_inc_split (0 = never)
 };
 
 struct LaunchCfg {
@@ -224,6 +228,7 @@ cudaError_t launch_cycle_dom(const DevGame &g, const LaunchCfg &lc, cudaStream_t
 cudaError_t launch_switch(const DevGame &g, bool odd, cudaStream_t s);
 cudaError_t launch_inc_iter(const DevGame &g, const LaunchCfg &lc, cudaStream_t s, int64_t nS);
 cudaError_t launch_even_inc(const DevGame &g, cudaStream_t s);
+cudaError_t launch_inc_split(const DevGame &g, cudaStream_t s);   // big-step continuation (ctl->split)
 cudaError_t launch_apply_all(const DevGame &g, cudaStream_t s);   // σ[S]/τ[S] of the exchanged S
 cudaError_t launch_val_bfs(const DevGame &g, const LaunchCfg &lc, cudaStream_t s);
 size_t children_scan_bytes(int64_t n1);

@@ -1502,6 +1502,63 @@ __device__ __forceinline__ void trace_ts(const DevGame &g, int k) {
     }
 }
 
+// V2 on D for the D-list entry i (step 3 of k_inc_iter; also the big-step kernel
+// k_inc_v2_split): walk from v through dirty vertices to the first clean vertex x (or
+// the sink) and merge the walk histogram into cpx[x] (exact, DESIGN.md "Compact
+// prefix"); after an All_Odd step also v's depth and its C mark; E by expand_rev.
+// Warp-uniform call sites (warp_append, expand_rev).
+__device__ __forceinline__ void inc_v2_item(const DevGame &g, int64_t i, int64_t nd, uint32_t ep, uint32_t cepoch,
+                                            bool odd_s, bool e_in_v2, uint8_t *hb, uint32_t *ow,
+                                            unsigned long long &wsteps) {
+    const int64_t N = g.n_int;
+    const uint32_t SINK = (uint32_t)N;
+    unsigned long long *jl = g.jl;
+    Ctl *ctl = g.ctl;
+    const int32_t v = i < nd ? __ldcg(g.Dl + i) : -1;
+    uint2 rr = make_uint2(0u, 0u);
+    if (e_in_v2 && v >= 0) rr = __ldcg(g.Dr + i);
+    if (odd_s) {
+        const bool addc = v >= 0 && __ldcg(g.cmark + v) != cepoch;
+        if (addc) g.cmark[v] = cepoch;
+        warp_append(addc, v, g.Cl, &ctl->nC);
+    }
+    if (v >= 0) {
+        bool fin = true;
+        if (!odd_s) {
+            const unsigned long long e = __ldcg(jl + v);
+            fin = (uint32_t)e == SINK;
+        }
+        g.top[v] = fin ? 0 : 1;
+        if (!fin) {
+            put_cpx(g, v, make_uint4(1u, 0, 0, 0), make_uint4(0, 0, 0, 0));
+        } else {
+            uint32_t mask = 0, steps = 0;
+            int32_t x = v;
+            while (x != (int32_t)N && __ldcg(g.dmark + x) == ep) {
+                const uint32_t p = __ldg(g.pidx + x);
+                x = __ldcg(g.succ + x);
+                if (++hb[p] == 255) { atomicOr(&ctl->inc_overflow, 1ull); break; }
+                mask |= 1u << p;
+                steps++;
+            }
+            wsteps += steps;
+            if (odd_s) {   // depth(v) = steps + depth(x); x is clean (final jl) or the sink
+                uint32_t dx = 0;
+                if (x != (int32_t)N) {
+                    const unsigned long long ex = __ldcg(jl + x);
+                    if ((uint32_t)ex != SINK) atomicOr(&ctl->inc_overflow, 1ull);   // clean ⊤ exit: redo in full
+                    dx = (uint32_t)(ex >> 32);
+                }
+                uint32_t dv = steps + dx;
+                if (dv > 0x7fffffffu) dv = 0x7fffffffu;
+                jl[v] = pack_jl(SINK, dv);
+            }
+            cpx_merge_store(g, v, hb, mask, x, ow);
+        }
+    }
+    if (e_in_v2) expand_rev<1>(g, -1, rr.x, rr.y, g.emark, ep, g.El, &ctl->nE);
+}
+
 __global__ void __launch_bounds__(kIncThreads) k_inc_iter(DevGame g) {
     __shared__ uint8_t hsm[kIncThreads][36];
     __shared__ uint32_t osm[kIncThreads][9];
@@ -1716,6 +1773,23 @@ __global__ void __launch_bounds__(kIncThreads) k_inc_iter(DevGame g) {
     }
     }
 
+    // Big steps continue in separate, fully occupied kernels (k_inc_v2_split, then the
+    // list-mode switch kernels and k_inc_split_fin; launched by the caller when
+    // ctl->split is set): this kernel's one 512-thread block per SM (128 registers,
+    // for the closure and the small steps) leaves the throughput phases latency-bound.
+    if (g.inc_split_min > 0 && nd >= g.inc_split_min) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            ctl->split = 1;
+            ctl->split_nd = (unsigned long long)nd;
+            ctl->split_ep = ep;
+            ctl->split_odd_s = odd_s ? 1u : 0u;
+            ctl->split_step = (unsigned long long)step;
+            ctl->nD = (unsigned long long)nd;
+            ctl->dlevels = (unsigned long long)levels;
+            ctl->v1_rounds = (unsigned long long)r;
+        }
+        return;
+    }
     // ---- 3. V2 on D (after an All_Odd step also V1's depth, and the C marks)
     trace_ts(g, 3);
     uint8_t *hb = hsm[threadIdx.x];
@@ -1727,52 +1801,8 @@ __global__ void __launch_bounds__(kIncThreads) k_inc_iter(DevGame g) {
     // reverse range is scanned right after its walk, saving a grid barrier and a
     // second pass over the D list
     const bool e_in_v2 = g.inc_e_in_v2 && !g.inc_fuse_e;
-    for (int64_t b0 = wbase; b0 < nd; b0 += stride) {   // warp-uniform (warp_append, expand_rev)
-        const int64_t i = b0 + lane;
-        const int32_t v = i < nd ? __ldcg(g.Dl + i) : -1;
-        uint2 rr = make_uint2(0u, 0u);
-        if (e_in_v2 && v >= 0) rr = __ldcg(g.Dr + i);
-        if (odd_s) {
-            const bool addc = v >= 0 && __ldcg(g.cmark + v) != cepoch;
-            if (addc) g.cmark[v] = cepoch;
-            warp_append(addc, v, g.Cl, &ctl->nC);
-        }
-        if (v >= 0) {
-            bool fin = true;
-            if (!odd_s) {
-                const unsigned long long e = __ldcg(jl + v);
-                fin = (uint32_t)e == SINK;
-            }
-            g.top[v] = fin ? 0 : 1;
-            if (!fin) {
-                put_cpx(g, v, make_uint4(1u, 0, 0, 0), make_uint4(0, 0, 0, 0));
-            } else {
-                uint32_t mask = 0, steps = 0;
-                int32_t x = v;
-                while (x != (int32_t)N && __ldcg(g.dmark + x) == ep) {
-                    const uint32_t p = __ldg(g.pidx + x);
-                    x = __ldcg(g.succ + x);
-                    if (++hb[p] == 255) { atomicOr(&ctl->inc_overflow, 1ull); break; }
-                    mask |= 1u << p;
-                    steps++;
-                }
-                wsteps += steps;
-                if (odd_s) {   // depth(v) = steps + depth(x); x is clean (final jl) or the sink
-                    uint32_t dx = 0;
-                    if (x != (int32_t)N) {
-                        const unsigned long long ex = __ldcg(jl + x);
-                        if ((uint32_t)ex != SINK) atomicOr(&ctl->inc_overflow, 1ull);   // clean ⊤ exit: redo in full
-                        dx = (uint32_t)(ex >> 32);
-                    }
-                    uint32_t dv = steps + dx;
-                    if (dv > 0x7fffffffu) dv = 0x7fffffffu;
-                    jl[v] = pack_jl(SINK, dv);
-                }
-                cpx_merge_store(g, v, hb, mask, x, ow);
-            }
-        }
-        if (e_in_v2) expand_rev<1>(g, -1, rr.x, rr.y, g.emark, ep, g.El, &ctl->nE);
-    }
+    for (int64_t b0 = wbase; b0 < nd; b0 += stride)   // warp-uniform (warp_append, expand_rev)
+        inc_v2_item(g, b0 + lane, nd, ep, cepoch, odd_s, e_in_v2, hb, ow, wsteps);
     gbar(ctl);
 
     // ---- 4. E = Odd vertices with a candidate in D: built by the closure scan
@@ -1867,6 +1897,41 @@ __global__ void __launch_bounds__(kIncThreads) k_inc_iter(DevGame g) {
     }
 }
 
+
+// The big-step continuation of k_inc_iter (ctl->split): V2 on D (+ E, C marks, depths)
+// at full occupancy; then k_switch<ODD> over E, its hard pass and k_apply_switches
+// (the list-mode kernels All_Even over C uses), then k_inc_split_fin.
+__global__ void __launch_bounds__(kThreads) k_inc_v2_split(DevGame g) {
+    __shared__ uint8_t hsm[kThreads][36];
+    __shared__ uint32_t osm[kThreads][9];
+    Ctl *ctl = g.ctl;
+    if (!__ldcg(&ctl->split)) return;
+    const int64_t nd = (int64_t)__ldcg(&ctl->split_nd);
+    const uint32_t ep = (uint32_t)__ldcg(&ctl->split_ep), cepoch = __ldcg(&ctl->lp_cepoch);
+    const bool odd_s = __ldcg(&ctl->split_odd_s) != 0;
+    const bool e_in_v2 = !g.inc_fuse_e;   // (E inside the closure scan otherwise)
+    uint8_t *hb = hsm[threadIdx.x];
+    uint32_t *ow = osm[threadIdx.x];
+#pragma unroll
+    for (int k = 0; k < 32; k++) hb[k] = 0;
+    unsigned long long wsteps = 0;
+    const int lane = threadIdx.x & 31;
+    const int64_t wbase = blockIdx.x * (int64_t)blockDim.x + threadIdx.x - lane;
+    for (int64_t b0 = wbase; b0 < nd; b0 += (int64_t)gridDim.x * blockDim.x)
+        inc_v2_item(g, b0 + lane, nd, ep, cepoch, odd_s, e_in_v2, hb, ow, wsteps);
+    wsteps = block_sum(wsteps);
+    if (threadIdx.x == 0 && wsteps) atomicAdd(&ctl->walk_steps, wsteps);
+}
+
+__global__ void k_inc_split_fin(Ctl *ctl) {
+    if (!ctl->split) return;
+    ctl->split = 0;
+    if (ctl->inc_overflow) return;   // walk overflow: nothing switched; the caller redoes the step in full
+    ctl->steps_done = ctl->split_step + 1;
+    ctl->last_sw = ctl->nswl;
+    ctl->nD_sum += ctl->split_nd;
+    ctl->nE_sum += ctl->nE;
+}
 
 // Incremental All_Even: E_even = Even vertices with a candidate in C (the union
 // of the dirty sets since the previous All_Even); no other Even decision can
@@ -2287,6 +2352,15 @@ cudaError_t launch_val_bfs(const DevGame &g, const LaunchCfg &lc, cudaStream_t s
 
 cudaError_t launch_apply_all(const DevGame &g, cudaStream_t s) {
     k_apply_switches<<<std::max(1, g_lc.sms * 4), kThreads, 0, s>>>(g, 1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_inc_split(const DevGame &g, cudaStream_t s) {
+    k_inc_v2_split<<<grid_for(g.n_int / 8 + 1, kThreads, 16), kThreads, 0, s>>>(g);
+    k_switch<true, false><<<std::max(1, g_lc.sms * 4), kThreads, 0, s>>>(g, g.El);
+    k_switch<true, true><<<std::max(1, g_lc.sms * 2), kThreads, 0, s>>>(g, nullptr);
+    k_apply_switches<<<std::max(1, g_lc.sms * 4), kThreads, 0, s>>>(g, 0);
+    k_inc_split_fin<<<1, 1, 0, s>>>(g.ctl);
     return cudaGetLastError();
 }
 

@@ -8,6 +8,7 @@
 //       k_inner_pre                                     inner cap; incremental or full; grid class
 //       SWITCH (h_mode) {
 //         LM_INC0..3: k_inc_iter (grid class 0..3)      incremental valuation(s) + All_Odd
+//                     IF (split) { V2 / E / All_Odd of a big step at full occupancy }
 //         LM_FULL:    V1, splitters, V2, All_Odd        from-scratch valuation + All_Odd
 //       }
 //       k_inner_post                                    counts; abort / overflow handling; S_Odd = ∅?
@@ -249,6 +250,9 @@ __global__ void k_even_post(LoopCfg cfg, Ctl *c, Handles h) {
     cudaGraphSetConditional(h.outer, cnt ? 1 : 0);
 }
 
+// IF handle of a big incremental step's continuation (k_inc_iter set ctl->split)
+__global__ void k_split_gate(Ctl *c, cudaGraphConditionalHandle h) { cudaGraphSetConditional(h, c->split ? 1 : 0); }
+
 cudaError_t add_kernel(cudaGraph_t graph, const cudaGraphNode_t *deps, size_t ndeps, void *fn, void **args,
                        cudaGraphNode_t *node) {
     cudaKernelNodeParams p = {};
@@ -355,6 +359,7 @@ cudaError_t build_loop_graph(const DevGame &g, const LaunchCfg &lc, const LoopCf
     cudaGraph_t body_i = b[0];
     GCK(cudaGraphConditionalHandleCreate(&h.mode, body_i, LM_NONE, cudaGraphCondAssignDefault));
     cudaGraphNode_t m1, m2, m3;
+    cudaGraphConditionalHandle h_split[4] = {};
     GCK(add_kernel(body_i, nullptr, 0, (void *)k_inner_pre, args, &m1));
     GCK(add_cond(body_i, &m1, 1, h.mode, cudaGraphCondTypeSwitch, 5, &m2, b));
     const std::vector<cudaGraph_t> mb = b;
@@ -362,6 +367,18 @@ cudaError_t build_loop_graph(const DevGame &g, const LaunchCfg &lc, const LoopCf
     for (int k = 0; k < 4 && !(omit & 1); k++) {   // incremental launches, one grid class each
         const int64_t nS = (int64_t)cfg.grid_class[k] * kIncThreads / std::max(1, cfg.inc_grid_mul);
         GCK(capture(cs, mb[k], [&] { return launch_inc_iter(g, lc, cs, std::max<int64_t>(1, nS)); }));
+        // then IF (ctl->split) { the big-step continuation, launch_inc_split }
+        cudaGraphNode_t kn;
+        size_t nn = 1;
+        GCK(cudaGraphGetNodes(mb[k], &kn, &nn));
+        GCK(cudaGraphConditionalHandleCreate(&h_split[k], mb[k], 0, cudaGraphCondAssignDefault));
+        void *gargs[] = {&ctl, &h_split[k]};
+        cudaGraphNode_t gate, ifn;
+        GCK(add_kernel(mb[k], &kn, 1, (void *)k_split_gate, gargs, &gate));
+        std::vector<cudaGraph_t> sb;
+        GCK(add_cond(mb[k], &gate, 1, h_split[k], cudaGraphCondTypeIf, 1, &ifn, sb));
+        GCK(capture(cs, sb[0], [&] { return launch_inc_split(g, cs); }));
+        count += 2 + 5;
     }
     GCK(capture(cs, mb[LM_FULL], [&] {
         int launches = 0;

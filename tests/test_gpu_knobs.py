@@ -43,6 +43,9 @@ def check(pg, g, ora, **kw):
     {"PGSI_INC_E_V2": "0"},                        # E built by a separate pass over D
     {"PGSI_INC_FUSE_E": "1"},                      # E built inside the closure scan
     {"PGSI_V2_DESIGN": "W"},                       # V2 by Wyllie over full rows (design comparison)
+    {"PGSI_INC_SPLIT": "1"},                       # every step continues in launch_inc_split
+    {"PGSI_INC_SPLIT": "1", "PGSI_DEVICE_LOOP": "2"},   # ... inside the device graph (IF node)
+    {"PGSI_INC_SPLIT": "0"},                       # never
     {"PGSI_INC_CLOSURE": "0"},                     # level-synchronous closure (grid barrier per level)
     {"PGSI_INC_CLO_CAP": "4"},                     # block-local closure: frontier / staging overflow
     {"PGSI_INC_CLO_CAP": "1", "PGSI_INC_GRID_MUL": "1"},   # every child overflows; tiny grids
