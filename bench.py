@@ -56,6 +56,9 @@ WORKLOADS = {
                  desc="F_deep(4M) closed-form family: one 4M-deep finite play, d=3 (BASELINE configs[3])"),
     "stair": dict(family="stair", L=5000, ref_iters=200, cpu_iters=400,
                   desc="F_stair(5000) long-iteration family: 5000 outer passes (BASELINE configs[4])"),
+    "stairs": dict(family="stairs", k=256, L=1000, ref_iters=100, cpu_iters=200,
+                   desc="256 copies of F_stair(1000): 256k vertices, 1000 outer passes, too large for the "
+                        "on-chip whole-solve kernels (BASELINE configs[4] long-iteration family at scale)"),
     "stair20k": dict(family="stair", L=20000, ref_iters=100, cpu_iters=200,
                      desc="F_stair(20000) long-iteration family: 20000 outer passes, too large for the "
                           "single-block kernel (BASELINE configs[4])"),
@@ -191,6 +194,8 @@ def make_game(wl, seed):
         return gi.elevator(wl["f"], wl["r"], seed)
     if fam == "stair":
         return gi.f_stair(wl["L"])
+    if fam == "stairs":
+        return gi.f_stairs(wl["k"], wl["L"])
     if fam == "deep":
         return gi.f_deep(wl["L"])
     return gi.random_game(wl["n"], wl["d"], wl["lo"], wl["hi"], seed)

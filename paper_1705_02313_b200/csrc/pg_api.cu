@@ -84,6 +84,7 @@ struct pg_game_s {
     // path pays tens of µs per iteration whatever the size, the cluster kernel pays per
     // vertex; scripts/cluster_probe.py); 2 = whenever the game fits
     int cluster_mode = 1;
+    int inc_even = 1;                 // PGSI_INC_EVEN=0: All_Even never inside k_inc_iter
     int64_t last_inner = 0;
     int smem_optin = 0;               // max dynamic shared memory per block (bytes)
     // Bellman-Ford arm (PG_BELLMAN_FORD): double-buffered key rows (⊤ = all INT_MAX)
@@ -849,6 +850,7 @@ pg_status solve_graph(pg_game h, int64_t *inner, int64_t *outer) {
         c.inc_ok = G.dp <= 32 && !(h->flags & PG_NO_INCREMENTAL);
         c.si_reset = (h->flags & PG_SI_RESET) != 0;
         c.inc_max_steps = (int32_t)std::min<int64_t>(h->inc_max_steps, 1 << 20);
+        c.even_in = c.inc_ok && !c.si_reset && h->inc_even;
         c.inc_grid_mul = std::max(1, G.inc_grid_mul);
         const int cap = std::max(1, h->lc.coop_inc);
         c.grid_class[0] = 1;
@@ -1143,11 +1145,13 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     h->inc_s_div_even = getenv("PGSI_INC_S_DIV_EVEN") ? atoi(getenv("PGSI_INC_S_DIV_EVEN")) : 64;
     h->inc_max_steps = getenv("PGSI_INC_STEPS") ? std::max(1, atoi(getenv("PGSI_INC_STEPS"))) : (1 << 20);
     G.inc_s_div = h->inc_s_div;
+    G.inc_s_div_even = h->inc_s_div_even;
     G.inc_grid_cap = h->lc.coop_inc;
     G.inc_grid_mul = getenv("PGSI_INC_GRID_MUL") ? atoi(getenv("PGSI_INC_GRID_MUL")) : 16;
     if (getenv("PGSI_SMALL_MAX")) h->small_max = atoll(getenv("PGSI_SMALL_MAX"));
     if (getenv("PGSI_CLUSTER_MAX")) h->cluster_max = atoll(getenv("PGSI_CLUSTER_MAX"));
     if (getenv("PGSI_CLUSTER")) h->cluster_mode = atoi(getenv("PGSI_CLUSTER"));
+    if (getenv("PGSI_INC_EVEN")) h->inc_even = atoi(getenv("PGSI_INC_EVEN"));
     if (getenv("PGSI_DEVICE_LOOP")) h->device_loop = atoi(getenv("PGSI_DEVICE_LOOP"));
     h->v2_wyllie = getenv("PGSI_V2_DESIGN") && (getenv("PGSI_V2_DESIGN")[0] == 'W' || getenv("PGSI_V2_DESIGN")[0] == 'w');
     if (h->v2_wyllie) h->device_loop = 0;   // the W path reads V1's depth back on the host

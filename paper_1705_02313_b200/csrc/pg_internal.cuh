@@ -66,6 +66,11 @@ struct Ctl {
     unsigned long long nE_sum;      // ... |E| summed over its steps
     unsigned long long cpx_gathers; // switch steps: 32 B prefix gathers after an undecided key compare
     unsigned long long nDl;         // incremental step: D-list length (block-local closure appends)
+    unsigned long long outer_done;  // k_inc_iter: All_Even steps it ran (outer passes completed)
+    unsigned long long even_sw_in;  // ... their Even switches, |E_even|, |C|
+    unsigned long long ne_even_in, nc_in;
+    unsigned long long end_kind;    // ... 0 after an Odd step with switches, 1 inner loop converged,
+                                    //     2 after an in-kernel All_Even with switches, 3 solve done
     unsigned long long split;       // k_inc_iter stopped after V1 on D: the caller runs launch_inc_split
     unsigned long long split_nd, split_ep, split_step;
     unsigned int split_odd_s, split_pad;
@@ -90,6 +95,10 @@ struct Ctl {
     unsigned int lp_cepoch;         // epoch of C (changes since the last All_Even)
     unsigned int lp_s_odd;          // the first step's switch list came from All_Odd
     unsigned int lp_max_steps;      // inner iterations the launch may run
+    unsigned int lp_even;           // k_inc_iter may run All_Even over C itself (device loop only)
+    unsigned int lp_c_valid;        // ... C covers every change since the last All_Even at launch start
+    long long lp_outer_left;        // ... outer passes it may still complete
+    unsigned int lp_cepoch_out;     // ... the C epoch after its last in-kernel All_Even
     // ---- device-resident Algorithm 1 (pg_loop.cu) ----
     long long ls_inner, ls_outer;   // valuations computed, outer passes (readings 11-12)
     unsigned long long ls_status;   // LS_RUNNING / LS_DONE / LS_CAP_INNER / LS_CAP_OUTER / LS_HOST_*
@@ -103,6 +112,7 @@ struct Ctl {
     unsigned int ls_epoch;          // last reserved D / E epoch
     unsigned int ls_cepoch;         // current C epoch
     unsigned int ls_resume;         // relaunch after a host fix: 1 = inside the inner loop, 2 = at All_Even
+    unsigned int ls_skip_even;      // k_inc_iter ran this pass's All_Even itself
     unsigned long long ls_st[24];   // statistics accumulators (LST_*)
 };
 #define PGSI_CTL_RESET_BYTES offsetof(pgsi::Ctl, bad_index)
@@ -166,6 +176,7 @@ struct DevGame {
     int32_t inc_grid_cap;   // cooperative grid cap of k_inc_iter
     int32_t inc_grid_mul;   // k_inc_iter grid = |S| * inc_grid_mul threads (capped)
     int64_t inc_s_div;      // incremental step only while |S| * inc_s_div <= n'
+    int64_t inc_s_div_even; // ... and |S| * inc_s_div_even <= n' when S came from All_Even
     int32_t inc_fuse_e;     // build E inside the dirty-closure scan (else a separate pass)
     int32_t inc_e_in_v2;    // build E in the V2-on-D pass (else a separate pass)
     int32_t inc_skip_v1;    // after All_Odd steps replace V1 on D by the V2 walk depth
@@ -203,6 +214,7 @@ struct LoopCfg {
     int32_t inc_ok;                 // incremental valuation allowed (dp <= 32, no PG_NO_INCREMENTAL)
     int32_t si_reset;               // PG_SI_RESET
     int32_t inc_max_steps;          // inner iterations per incremental launch
+    int32_t even_in;                // k_inc_iter may run All_Even over C itself (PGSI_INC_EVEN)
     int32_t inc_grid_mul;           // k_inc_iter grid = |S| * mul threads
     int32_t grid_class[4];          // k_inc_iter grid sizes of the SWITCH bodies LM_INC0..3
     int32_t K;                      // splitter stride (statistics)

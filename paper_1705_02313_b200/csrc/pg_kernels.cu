@@ -971,6 +971,8 @@ __device__ __noinline__ int cmp_full(const DevGame &g, int32_t a, int32_t b) {
     return 0;
 }
 
+__device__ __forceinline__ bool sh_active(const DevGame &g) { return g.sharded != 0; }
+
 // Vertex v is in this rank's switch shard (always true when world = 1).
 __device__ __forceinline__ bool sh_owns(const DevGame &g, int64_t v) {
     return v < g.n_even ? (v >= g.sh_even_lo && v < g.sh_even_hi) : (v >= g.sh_odd_lo && v < g.sh_odd_hi);
@@ -1573,10 +1575,19 @@ __global__ void __launch_bounds__(kIncThreads) k_inc_iter(DevGame g) {
     // Consecutive inner iterations run in this one launch (Algorithm 1's inner
     // loop, kept on the device) while each stays incremental;
     // step t uses epoch lp_epoch + t for its D / E marks (reserved by the caller).
-    const uint32_t epoch0 = __ldcg(&ctl->lp_epoch), cepoch = __ldcg(&ctl->lp_cepoch);
-    const uint32_t s_odd = __ldcg(&ctl->lp_s_odd), max_steps = __ldcg(&ctl->lp_max_steps);
+    const uint32_t epoch0 = __ldcg(&ctl->lp_epoch);
+    uint32_t cepoch = __ldcg(&ctl->lp_cepoch);
+    const uint32_t max_steps = __ldcg(&ctl->lp_max_steps);
+    // In-kernel All_Even (step 9, lp_even; the device loop only): when a step converges
+    // (no Odd switch: τ = br(σ)) and C still covers every change since the last All_Even,
+    // All_Even over C runs here and the next best response starts in the same launch.
+    // Each step then uses two epochs (D / E, then E_even), reserved by the caller.
+    const bool even_in = __ldcg(&ctl->lp_even) != 0;
+    bool c_valid = __ldcg(&ctl->lp_c_valid) != 0;
+    long long outer_left = (long long)__ldcg(&ctl->lp_outer_left);
+    bool s_from_odd = __ldcg(&ctl->lp_s_odd) != 0;   // this step's S came from All_Odd
     for (int step = 0;; step++) {
-    const uint32_t ep = epoch0 + (uint32_t)step;
+    const uint32_t ep = epoch0 + (uint32_t)step * (even_in ? 2u : 1u);
     if (blockIdx.x == 0 && threadIdx.x == 0) ctl->steps_done = (unsigned long long)step;
     trace_ts(g, 0);
     // ---- 1. dirty closure
@@ -1589,7 +1600,7 @@ __global__ void __launch_bounds__(kIncThreads) k_inc_iter(DevGame g) {
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) ctl->nDl = (unsigned long long)ns;
     gbar(ctl);
-    if (blockIdx.x == 0 && threadIdx.x == 0) { ctl->nswl = 0; ctl->nhard = 0; }  // step 5 appends anew
+    if (blockIdx.x == 0 && threadIdx.x == 0) { ctl->nswl = 0; ctl->nhard = 0; ctl->nE = 0; }  // steps 4-5 append anew
     int64_t lo = 0, hi = ns;
     int levels = 0;
     if (g.inc_closure == 1) {
@@ -1720,7 +1731,7 @@ __global__ void __launch_bounds__(kIncThreads) k_inc_iter(DevGame g) {
     // walk: depth(v) = walk length + depth(x) at the first clean vertex x. (A walk
     // ending at a clean ⊤ vertex would contradict this; it sets inc_overflow and the
     // host redoes the step in full, so results never depend on the argument.)
-    const bool odd_s = (step > 0 || s_odd) && g.inc_skip_v1;
+    const bool odd_s = s_from_odd && g.inc_skip_v1;
     unsigned long long *jl = g.jl;
     int r = 0;
     if (!odd_s) {
@@ -1889,11 +1900,85 @@ __global__ void __launch_bounds__(kIncThreads) k_inc_iter(DevGame g) {
         ctl->newfin[0] = ctl->newfin[1] = ctl->newfin[2] = 0;
         ctl->nE = 0;
     }
-    const int64_t need = (nsn * g.inc_grid_mul + kIncThreads - 1) / kIncThreads;   // the grid the host would pick
-    if (sw == 0 || step + 1 >= (int)max_steps || nsn * g.inc_s_div > N ||
+    if (sw != 0) {
+        s_from_odd = true;
+        const int64_t need = (nsn * g.inc_grid_mul + kIncThreads - 1) / kIncThreads;   // the grid the host would pick
+        if (step + 1 >= (int)max_steps || nsn * g.inc_s_div > N ||
+            (need > (int64_t)gridDim.x && (int)gridDim.x < g.inc_grid_cap)) {
+            if (blockIdx.x == 0 && threadIdx.x == 0) ctl->end_kind = 0;
+            return;
+        }
+        gbar(ctl);   // the resets above precede the next step's appends
+        continue;
+    }
+    // ---- 9. S_Odd = ∅: the best response is final. All_Even over C here (
+    // the same kernels' logic as launch_even_inc) when allowed, else back to the caller.
+    const int64_t nc = (int64_t)bcast_ld(&ctl->nC);
+    if (!even_in || !c_valid || nc * 8 > N || sh_active(g)) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) ctl->end_kind = 1;
+        return;
+    }
+    gbar(ctl);   // the step-8 resets are visible; nobody reads nswl / nhard / nE any more
+    if (blockIdx.x == 0 && threadIdx.x == 0) { ctl->nswl = 0; ctl->nhard = 0; ctl->nE = 0; }
+    gbar(ctl);
+    const uint32_t ep_e = ep + 1;   // E_even marks: Even predecessors of C
+    for (int64_t b0 = wbase; b0 < nc; b0 += stride) {
+        const int64_t i = b0 + lane;
+        uint32_t rb = 0, re = 0;
+        if (i < nc) {
+            const int32_t f = __ldcg(g.Cl + i);
+            rb = __ldg(g.rrp + f);
+            re = __ldg(g.rrp + f + 1);
+        }
+        expand_rev<2>(g, -1, rb, re, g.emark, ep_e, g.El, &ctl->nE);
+    }
+    gbar(ctl);
+    const int64_t nee = (int64_t)bcast_ld(&ctl->nE);
+    unsigned long long ereads = 0, efulls = 0, epref = 0;
+    for (int64_t i = tid; i < nee; i += stride) {
+        const int64_t v = __ldcg(g.El + i);
+        if (switch_vertex<false, false>(g, v, cpx, ereads, efulls, epref) == 2)
+            g.hard[atomicAdd(&ctl->nhard, 1ull)] = (int32_t)v;
+    }
+    gbar(ctl);
+    const int64_t nhe = (int64_t)bcast_ld(&ctl->nhard);
+    for (int64_t i = tid; i < nhe; i += stride) {
+        const int64_t v = __ldcg(g.hard + i);
+        switch_vertex<false, true>(g, v, cpx, ereads, efulls, epref);
+    }
+    gbar(ctl);
+    const int64_t nes = (int64_t)bcast_ld(&ctl->nswl);   // σ := σ[All_Even]; it is S of the next step
+    for (int64_t i = tid; i < nes; i += stride) {
+        const int2 e = __ldcg(g.swl + i);
+        g.succ[e.x] = e.y;
+    }
+    t = block_sum(ereads);
+    if (threadIdx.x == 0 && t) atomicAdd(&ctl->rows_even, t);
+    t = block_sum(epref);
+    if (threadIdx.x == 0 && t) atomicAdd(&ctl->cpx_gathers, t);
+    t = block_sum(efulls);
+    if (threadIdx.x == 0 && t) atomicAdd(&ctl->full_even, t);
+    gbar(ctl);   // the even list is applied before the next step's closure reads succ
+    cepoch++;    // a new C starts: changes after this All_Even
+    c_valid = true;
+    outer_left--;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        ctl->outer_done += 1;
+        ctl->even_sw_in += (unsigned long long)nes;
+        ctl->ne_even_in += (unsigned long long)nee;
+        ctl->nc_in += (unsigned long long)nc;
+        ctl->nC = 0;
+        ctl->lp_cepoch_out = cepoch;
+        ctl->step_sw[(step + 1) & 1] = 0;
+        ctl->end_kind = nes == 0 ? 3 : 2;
+    }
+    if (nes == 0) return;   // S_Even = ∅: σ is optimal; the solve is done
+    s_from_odd = false;
+    const int64_t need = (nes * g.inc_grid_mul + kIncThreads - 1) / kIncThreads;
+    if (outer_left <= 0 || step + 1 >= (int)max_steps || nes * g.inc_s_div_even > N ||
         (need > (int64_t)gridDim.x && (int)gridDim.x < g.inc_grid_cap))
         return;
-    gbar(ctl);   // the resets above precede the next step's appends
+    gbar(ctl);
     }
 }
 
@@ -1929,6 +2014,7 @@ __global__ void k_inc_split_fin(Ctl *ctl) {
     if (ctl->inc_overflow) return;   // walk overflow: nothing switched; the caller redoes the step in full
     ctl->steps_done = ctl->split_step + 1;
     ctl->last_sw = ctl->nswl;
+    ctl->end_kind = 0;
     ctl->nD_sum += ctl->split_nd;
     ctl->nE_sum += ctl->nE;
 }
@@ -2390,6 +2476,9 @@ __global__ void k_set_launch_params(Ctl *ctl, uint32_t epoch, uint32_t cepoch, u
     ctl->lp_cepoch = cepoch;
     ctl->lp_s_odd = s_odd;
     ctl->lp_max_steps = max_steps;
+    ctl->lp_even = 0;   // the host-driven loop runs All_Even itself
+    ctl->lp_c_valid = 0;
+    ctl->lp_outer_left = 0;
 }
 
 cudaError_t launch_set_launch_params(Ctl *ctl, uint32_t epoch, uint32_t cepoch, uint32_t s_odd, uint32_t max_steps,

@@ -61,6 +61,7 @@ __global__ void k_loop_init(Ctl *c, uint32_t epoch, uint32_t cepoch) {
     c->ls_epoch = epoch;
     c->ls_cepoch = cepoch;
     c->ls_resume = 0;
+    c->ls_skip_even = 0;
     for (int k = 0; k < 24; k++) c->ls_st[k] = 0;
 }
 
@@ -114,7 +115,8 @@ __global__ void k_inner_pre(LoopCfg cfg, Ctl *c, Handles h) {
         long long steps = cfg.inc_max_steps;
         if (cfg.max_inner > 0) steps = min(steps, cfg.max_inner - c->ls_inner);
         steps = max(1ll, min(steps, (long long)(1 << 20)));
-        if (c->ls_epoch > 0xffffffffu - (unsigned int)steps - 2u) {   // marks would wrap: host clears them
+        const unsigned int per = cfg.even_in ? 2u : 1u;   // epochs per step (D / E, then E_even)
+        if (c->ls_epoch > 0xffffffffu - per * (unsigned int)steps - 2u) {   // marks would wrap: host clears them
             c->ls_status = LS_HOST_EPOCHS;
             c->ls_resume = 1;
             c->ls_mode = LM_NONE;
@@ -123,10 +125,13 @@ __global__ void k_inner_pre(LoopCfg cfg, Ctl *c, Handles h) {
             return;
         }
         c->lp_epoch = c->ls_epoch + 1;
-        c->ls_epoch += (unsigned int)steps;
+        c->ls_epoch += per * (unsigned int)steps;
         c->lp_cepoch = c->ls_cepoch;
         c->lp_s_odd = c->ls_last_sw_odd;
         c->lp_max_steps = (unsigned int)steps;
+        c->lp_even = cfg.even_in;
+        c->lp_c_valid = c->ls_c_valid;
+        c->lp_outer_left = cfg.max_outer > 0 ? cfg.max_outer - c->ls_outer : 0x7fffffffffffffffll;
         const long long need = ((long long)nsw * cfg.inc_grid_mul + kIncThreads - 1) / kIncThreads;
         mode = LM_INC3;
         for (int k = 0; k < 4; k++)
@@ -158,6 +163,17 @@ __global__ void k_inner_post(LoopCfg cfg, Ctl *c, Handles h) {
         st_add(c, LST_WALK, c->walk_steps);
         st_add(c, LST_V1_ROUNDS, c->v1_rounds);
         c->ls_inner += (long long)done;
+        const unsigned long long od = c->outer_done;   // All_Even steps k_inc_iter ran itself
+        if (od) {
+            c->ls_outer += (long long)od;
+            c->ls_cepoch = c->lp_cepoch_out;
+            c->ls_c_valid = 1;
+            st_add(c, LST_EVEN_SW, c->even_sw_in);
+            st_add(c, LST_EVEN_INC, od);
+            st_add(c, LST_NE_EVEN, c->ne_even_in);
+            st_add(c, LST_NC, c->nc_in);
+            st_add(c, LST_ROWS_EVEN, c->rows_even);
+        }
         if (c->inc_overflow) {   // closure too deep / large or walk too long: redo this step in full
             st_add(c, LST_INC_ABORTS, 1);
             c->ls_force_full = 1;
@@ -165,10 +181,22 @@ __global__ void k_inner_post(LoopCfg cfg, Ctl *c, Handles h) {
             return;
         }
         c->ls_last_nsw = c->nswl;
-        c->ls_last_sw_odd = 1;
         c->ls_have_state = 1;
         c->ls_force_full = 0;
-        cudaGraphSetConditional(h.inner, c->last_sw ? 1 : 0);
+        const unsigned long long ek = od ? c->end_kind : (c->last_sw ? 0ull : 1ull);
+        if (ek == 3) {                        // an in-kernel All_Even made no switch: done
+            c->ls_status = LS_DONE;
+            cudaGraphSetConditional(h.inner, 0);
+            return;
+        }
+        if (ek == 2) {                        // it stopped right after an All_Even with switches
+            c->ls_last_sw_odd = 0;
+            c->ls_skip_even = 1;
+            cudaGraphSetConditional(h.inner, 0);
+            return;
+        }
+        c->ls_last_sw_odd = 1;
+        cudaGraphSetConditional(h.inner, ek == 0 ? 1 : 0);
         return;
     }
     if (c->spl_overflow) {   // the host grows the splitter buffers and relaunches
@@ -200,7 +228,7 @@ __global__ void k_inner_post(LoopCfg cfg, Ctl *c, Handles h) {
 // All_Even over C when every valuation since the previous All_Even was incremental
 // and C is small (pg_api.cu even_switch), else over all Even vertices.
 __global__ void k_even_pre(LoopCfg cfg, Ctl *c, Handles h) {
-    if (c->ls_status != LS_RUNNING) {
+    if (c->ls_status != LS_RUNNING || c->ls_skip_even) {
         cudaGraphSetConditional(h.even, 2);
         return;
     }
@@ -226,6 +254,11 @@ __global__ void k_even_pre(LoopCfg cfg, Ctl *c, Handles h) {
 }
 
 __global__ void k_even_post(LoopCfg cfg, Ctl *c, Handles h) {
+    if (c->ls_skip_even) {   // k_inc_iter ran (and counted) this pass's All_Even
+        c->ls_skip_even = 0;
+        cudaGraphSetConditional(h.outer, c->ls_status == LS_RUNNING ? 1 : 0);
+        return;
+    }
     if (c->ls_status != LS_RUNNING) {
         cudaGraphSetConditional(h.outer, 0);
         return;

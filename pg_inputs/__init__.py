@@ -15,6 +15,7 @@ from .games import (  # noqa: F401
     counter_hash,
     random_game,
     f_stair,
+    f_stairs,
     f_deep,
     f_oddchain,
     ladder,

@@ -129,6 +129,16 @@ def f_stair(L: int) -> Game:
     return Game(np.arange(L + 1, dtype=np.int64), col, owner, pri, f"stair-{L}")
 
 
+def f_stairs(k: int, L: int) -> Game:
+    """k disjoint copies of F_stair(L) (copy c holds ids c*L .. c*L+L-1): a long-iteration
+    game of any size (n = k*L, outer passes max(L, 2); the copies advance in lockstep)."""
+    one = f_stair(L)
+    off = (np.arange(k, dtype=np.int64) * L)[:, None]
+    col = (one.col.astype(np.int64)[None, :] + off).reshape(-1).astype(np.int32)
+    return Game(np.arange(k * L + 1, dtype=np.int64), col, np.tile(one.owner, k), np.tile(one.priority, k),
+                f"stairs-{k}x{L}")
+
+
 def f_deep(L: int) -> Game:
     """SURVEY.md App. A F_deep(L): e_0..e_{L-1} Even pri 2, e_i -> e_{i+1},
     e_{L-1} -> o; o = L is Odd pri 3 with a self-loop."""

@@ -135,3 +135,24 @@ def test_device_loop_epoch_wrap(pg, monkeypatch):
             monkeypatch.setenv("PGSI_DEVICE_LOOP", loop)
             r = pg.Game.from_game(g).solve(want_val=True)
             same(r, ora, g.n)
+
+
+@pytest.mark.parametrize("k,L", [(64, 300), (1, 4000), (500, 40)])
+def test_device_loop_long_iteration_stairs(pg, monkeypatch, k, L):
+    """Many copies of F_stair(L) (too large for the on-chip kernels at k = 64): L outer
+    passes whose All_Even steps run inside k_inc_iter; the closed form and the oracle."""
+    monkeypatch.setenv("PGSI_SMALL_MAX", "0")
+    monkeypatch.setenv("PGSI_CLUSTER", "0")
+    monkeypatch.setenv("PGSI_DEVICE_LOOP", "2")
+    g = gi.f_stairs(k, L)
+    ora = Oracle(g).solve()
+    assert ora.outer_passes == max(L, 2)
+    r = pg.Game.from_game(g).solve(want_val=True)
+    assert r.stats["device_loop_solves"] == 1
+    same(r, ora, g.n)
+    for cap in (L // 2, L - 1):   # outer caps land inside in-kernel All_Even sequences
+        with pytest.raises(pg.PGError) as e:
+            pg.Game.from_game(g, max_outer=cap).solve()
+        assert e.value.name == "PG_EITERCAP"
+    r = pg.Game.from_game(g, max_outer=max(L, 2)).solve(want_val=True)
+    same(r, ora, g.n)

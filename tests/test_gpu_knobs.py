@@ -46,6 +46,8 @@ def check(pg, g, ora, **kw):
     {"PGSI_INC_SPLIT": "1"},                       # every step continues in launch_inc_split
     {"PGSI_INC_SPLIT": "1", "PGSI_DEVICE_LOOP": "2"},   # ... inside the device graph (IF node)
     {"PGSI_INC_SPLIT": "0"},                       # never
+    {"PGSI_INC_EVEN": "0", "PGSI_DEVICE_LOOP": "2"},   # All_Even never inside k_inc_iter
+    {"PGSI_INC_STEPS": "3", "PGSI_DEVICE_LOOP": "2"},  # in-kernel All_Even cut short by the step budget
     {"PGSI_INC_CLOSURE": "0"},                     # level-synchronous closure (grid barrier per level)
     {"PGSI_INC_CLO_CAP": "4"},                     # block-local closure: frontier / staging overflow
     {"PGSI_INC_CLO_CAP": "1", "PGSI_INC_GRID_MUL": "1"},   # every child overflows; tiny grids

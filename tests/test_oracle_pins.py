@@ -504,3 +504,14 @@ def test_trace_consistent_with_solve(seed):
     # identical solve outputs with and without the trace
     np.testing.assert_array_equal(t.tau, r.tau)
     np.testing.assert_array_equal(t.val, r.val)
+
+
+@pytest.mark.parametrize("k,L", [(1, 5), (3, 7), (5, 2), (4, 1)])
+def test_stairs_closed_form(k, L):
+    """k disjoint copies of F_stair(L): the copies switch in lockstep, so
+    outer passes = inner iterations = max(L, 2), W_Even = V, σ*(e_i) = e_{i+1} per copy."""
+    g = gi.f_stairs(k, L)
+    r = Oracle(g).solve()
+    assert r.outer_passes == max(L, 2) and r.inner_iters == max(L, 2)
+    assert (r.winner == 0).all()
+    assert list(r.sigma) == [c * L + min(i + 1, L - 1) for c in range(k) for i in range(L)]
