@@ -85,6 +85,10 @@ struct pg_game_s {
     // vertex; scripts/cluster_probe.py); 2 = whenever the game fits
     int cluster_mode = 1;
     int inc_even = 1;                 // PGSI_INC_EVEN=0: All_Even never inside k_inc_iter
+    int cluster_C = -1;               // planned cluster size (-1 = not planned yet, 0 = does not fit)
+    int64_t cluster_colcap = 0;       // ... and its per-CTA edge capacity
+    int cluster_min = 8;              // smallest cluster the whole-solve cluster kernel uses (PGSI_CLUSTER_CTAS;
+                                      // 8 measured fastest on F_stair(20000): 2 / 4 / 8 / 16 CTAs 14.6 / 14.6 / 11.3 / 13.1 µs per pass)
     int64_t last_inner = 0;
     int smem_optin = 0;               // max dynamic shared memory per block (bytes)
     // Bellman-Ford arm (PG_BELLMAN_FORD): double-buffered key rows (⊤ = all INT_MAX)
@@ -1152,6 +1156,7 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     if (getenv("PGSI_CLUSTER_MAX")) h->cluster_max = atoll(getenv("PGSI_CLUSTER_MAX"));
     if (getenv("PGSI_CLUSTER")) h->cluster_mode = atoi(getenv("PGSI_CLUSTER"));
     if (getenv("PGSI_INC_EVEN")) h->inc_even = atoi(getenv("PGSI_INC_EVEN"));
+    if (getenv("PGSI_CLUSTER_CTAS")) h->cluster_min = atoi(getenv("PGSI_CLUSTER_CTAS"));
     if (getenv("PGSI_DEVICE_LOOP")) h->device_loop = atoi(getenv("PGSI_DEVICE_LOOP"));
     h->v2_wyllie = getenv("PGSI_V2_DESIGN") && (getenv("PGSI_V2_DESIGN")[0] == 'W' || getenv("PGSI_V2_DESIGN")[0] == 'w');
     if (h->v2_wyllie) h->device_loop = 0;   // the W path reads V1's depth back on the host
@@ -1469,16 +1474,28 @@ pg_status pg_solve(pg_game h, uint8_t *winner, int32_t *sigma, int32_t *tau, int
         // too large for one block: the whole solve on one thread-block cluster (up to 16
         // SMs' shared memory) when the state fits there
         const bool cluster_want = h->cluster_mode == 2 || (h->cluster_mode == 1 && h->last_inner * 4 >= h->G.n_int);
-        const int cluster_C = (!small && cluster_want && h->G.n_int + 1 <= h->cluster_max && !dist_active(h) &&
-                               !check && !h->trace &&
-                               !(h->flags & (PG_BELLMAN_FORD | PG_TRACE | PG_PHASE_TIMING | PG_BFS)))
-                                  ? cluster_size_for(h->G.n_int, h->G.dp, (size_t)h->smem_optin - 1024)
-                                  : 0;
+        int cluster_C = 0;
+        if (!small && cluster_want && h->G.n_int + 1 <= h->cluster_max && !dist_active(h) && !check && !h->trace &&
+            !(h->flags & (PG_BELLMAN_FORD | PG_TRACE | PG_PHASE_TIMING | PG_BFS))) {
+            if (h->cluster_C < 0) {   // plan once per handle: needs the CSR offsets on the host
+                h->cluster_C = 0;
+                const size_t smem = (size_t)h->smem_optin - 1024;
+                if ((h->G.n_int + 1) * (8 * (int64_t)h->G.dp + 13) <= 16 * (int64_t)smem) {
+                    std::vector<uint32_t> rp((size_t)h->G.n_int + 1);
+                    CK(h, cudaMemcpyAsync(rp.data(), h->G.rp, sizeof(uint32_t) * rp.size(), cudaMemcpyDeviceToHost,
+                                          h->stream));
+                    CK(h, cudaStreamSynchronize(h->stream));
+                    h->cluster_C = cluster_size_for(h->G.n_int, h->G.dp, smem, h->cluster_min, rp.data(),
+                                                    &h->cluster_colcap);
+                }
+            }
+            cluster_C = h->cluster_C;
+        }
         if (cluster_C) {
             {
                 PhaseScope ps(h, PH_OTHER);
-                CK(h, launch_solve_cluster(h->G, cluster_C, (h->flags & PG_SI_RESET) != 0, h->max_inner,
-                                           h->max_outer, h->stream));
+                CK(h, launch_solve_cluster(h->G, cluster_C, h->cluster_colcap, (h->flags & PG_SI_RESET) != 0,
+                                           h->max_inner, h->max_outer, h->stream));
                 h->st.gpu_launches += 1;
             }
             if ((rc = readback(h))) return rc;

@@ -253,9 +253,10 @@ cudaError_t launch_solve_small(const DevGame &g, bool check, bool reset, int64_t
                                cudaStream_t s);
 cudaError_t launch_bf_init(int32_t *rows0, int32_t *rows1, int64_t count, int sms, cudaStream_t s);
 // the same on a thread-block cluster of C CTAs with distributed shared memory (pg_small.cu)
-int cluster_size_for(int64_t n_int, int dp, size_t smem_per_cta);
-cudaError_t launch_solve_cluster(const DevGame &g, int C, bool reset, int64_t max_inner, int64_t max_outer,
-                                 cudaStream_t s);
+int cluster_size_for(int64_t n_int, int dp, size_t smem_per_cta, int min_ctas, const uint32_t *rp_host,
+                     int64_t *col_cap);
+cudaError_t launch_solve_cluster(const DevGame &g, int C, int64_t col_cap, bool reset, int64_t max_inner,
+                                 int64_t max_outer, cudaStream_t s);
 cudaError_t launch_export_val(const DevGame &g, int64_t count, int32_t *val_out, uint8_t *top_out,
                               cudaStream_t s);
 cudaError_t launch_export_strategy(const DevGame &g, int64_t count, int32_t *out, int which,

@@ -241,26 +241,48 @@ namespace cg = cooperative_groups;
 
 struct ClusterLayout {   // offsets inside each CTA's dynamic shared memory; S = vertices per CTA
     int32_t S, C;
-    size_t rows[2], J[2], top, total;
+    int64_t col_cap;        // most out-edges of one CTA's vertices
+    // rows / J of the Wyllie rounds (⊤ = J still short of the sink after the last round), and
+    // the CTA's own slice of the game: CSR offsets (relative), successors, priority indices, profile
+    size_t rows[2], J[2], rp, col, pidx, succ, oddp, total;
 };
 
-static ClusterLayout cluster_layout(int64_t n1, int dp, int C) {
+static ClusterLayout cluster_layout(int64_t n1, int dp, int C, int64_t col_cap) {
     ClusterLayout L{};
     L.C = C;
     L.S = (int32_t)((n1 + C - 1) / C);
+    L.col_cap = col_cap;
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 15) & ~size_t(15); return o; };
     for (int b = 0; b < 2; b++) L.rows[b] = take((size_t)L.S * dp * 4);
     for (int b = 0; b < 2; b++) L.J[b] = take((size_t)L.S * 4);
-    L.top = take((size_t)L.S);
+    L.rp = take(((size_t)L.S + 1) * 4);
+    L.col = take((size_t)col_cap * 4);
+    L.succ = take((size_t)L.S * 4);
+    L.pidx = take((size_t)L.S);
+    L.oddp = take((size_t)std::max(dp, 32));
     L.total = off;
     return L;
 }
 
-// smallest cluster size (2..16) whose per-CTA state fits smem_per_cta; 0 if none
-int cluster_size_for(int64_t n_int, int dp, size_t smem_per_cta) {
-    for (int C = 2; C <= 16; C *= 2)
-        if (cluster_layout(n_int + 1, dp, C).total <= smem_per_cta) return C;
+// smallest cluster size (min_ctas..16) whose per-CTA state fits smem_per_cta; 0 if none.
+// rp_host = the device-order CSR offsets (n_int + 1 entries); *col_cap receives the
+// largest per-CTA edge count of the chosen size.
+int cluster_size_for(int64_t n_int, int dp, size_t smem_per_cta, int min_ctas, const uint32_t *rp_host,
+                     int64_t *col_cap) {
+    const int64_t n1 = n_int + 1;
+    for (int C = std::max(2, min_ctas); C <= 16; C *= 2) {
+        const int64_t S = (n1 + C - 1) / C;
+        int64_t cap = 0;
+        for (int r = 0; r < C; r++) {
+            const int64_t lo = std::min<int64_t>(r * S, n_int), hi = std::min<int64_t>(lo + S, n_int);
+            cap = std::max<int64_t>(cap, (int64_t)rp_host[hi] - (int64_t)rp_host[lo]);
+        }
+        if (cluster_layout(n1, dp, C, cap).total <= smem_per_cta) {
+            *col_cap = cap;
+            return C;
+        }
+    }
     return 0;
 }
 
@@ -289,11 +311,29 @@ __global__ void __launch_bounds__(kSmallThreads) k_solve_cluster(DevGame g, Clus
     char *base = reinterpret_cast<char *>(smem4);
     int32_t *const rowsL[2] = {reinterpret_cast<int32_t *>(base + L.rows[0]), reinterpret_cast<int32_t *>(base + L.rows[1])};
     int32_t *const JL[2] = {reinterpret_cast<int32_t *>(base + L.J[0]), reinterpret_cast<int32_t *>(base + L.J[1])};
-    uint8_t *const topL = reinterpret_cast<uint8_t *>(base + L.top);
+    uint32_t *const rpL = reinterpret_cast<uint32_t *>(base + L.rp);
+    int32_t *const colL = reinterpret_cast<int32_t *>(base + L.col);
+    int32_t *const succL = reinterpret_cast<int32_t *>(base + L.succ);
+    uint8_t *const pidxL = reinterpret_cast<uint8_t *>(base + L.pidx);
+    uint8_t *const oddL = reinterpret_cast<uint8_t *>(base + L.oddp);
     const int32_t N = (int32_t)g.n_int, SINK = N, S = L.S;
     const int dp = g.dp;
     const int t = threadIdx.x, T = blockDim.x;
     const int32_t lo = r * S, hi = min(lo + S, N + 1);   // this CTA's vertices (the sink is the last)
+    const int32_t hiv = min(hi, N);                      // ... without the sink
+    // the CTA's own slice of the game in shared memory: no global load inside the loop
+    {
+        const uint32_t e_lo = lo <= N ? g.rp[lo] : 0u;
+        for (int32_t v = lo + t; v <= hiv; v += T) rpL[v - lo] = g.rp[v] - e_lo;
+        const uint32_t ne = lo < N ? g.rp[hiv] - e_lo : 0u;
+        for (uint32_t e = t; e < ne; e += T) colL[e] = g.col[e_lo + e];
+        for (int32_t v = lo + t; v < hiv; v += T) {
+            succL[v - lo] = g.succ[v];
+            pidxL[v - lo] = g.pidx[v];
+        }
+        for (int i = t; i < dp; i += T) oddL[i] = g.oddp[i];
+        __syncthreads();
+    }
     // the CTA-local pointer of vertex w's entry in a per-vertex array at local offset `a`
     auto rowp = [&](int b, int32_t w) -> const int32_t * {
         const int o = w / S;
@@ -303,10 +343,9 @@ __global__ void __launch_bounds__(kSmallThreads) k_solve_cluster(DevGame g, Clus
         const int o = w / S;
         return cl.map_shared_rank(JL[b], o) + (w - o * S);
     };
-    auto topv = [&](int32_t w) -> bool {
-        const int o = w / S;
-        return *(cl.map_shared_rank(topL, o) + (w - o * S)) != 0;
-    };
+    int cur = 0;   // buffer holding the final rows / J of the last valuation
+    // ⊤ = still unfinished after the last Wyllie round: J(w) != sink (no separate pass)
+    auto topv = [&](int32_t w) -> bool { return *jp(cur, w) != SINK; };
     // a ⊏ b on (row, ⊤) pairs of buffer b_; the sink is the finite zero row
     auto less = [&](int b_, int32_t a, int32_t b) -> bool {
         const bool ta = a != SINK && topv(a), tb = b != SINK && topv(b);
@@ -322,20 +361,20 @@ __global__ void __launch_bounds__(kSmallThreads) k_solve_cluster(DevGame g, Clus
     int parity = 0;
     int64_t inner = 0, outer = 0, rounds = 0, odd_sw = 0, even_sw = 0;
     int status = 0;
-    int cur = 0;
+    const bool has_odd = g.n_even < N;
     for (;;) {                                                        // Algorithm 1, outer repeat
         if (max_outer > 0 && outer >= max_outer) { status = 1; break; }
         if (reset && outer > 0) {                                     // SI-Reset: τ := τ_init
-            for (int32_t v = max(lo, (int32_t)g.n_even) + t; v < min(hi, N); v += T) g.succ[v] = g.col[g.rp[v]];
+            for (int32_t v = max(lo, (int32_t)g.n_even) + t; v < hiv; v += T) succL[v - lo] = colL[rpL[v - lo]];
             cl.sync();
         }
         bool stop = false;
         for (;;) {                                                    // inner repeat
             if (max_inner > 0 && inner >= max_inner) { status = 1; stop = true; break; }
             for (int32_t v = lo + t; v < hi; v += T) {                // round 0 = (succ, e_pri)
-                const int p = v < N ? g.pidx[v] : -1;
-                for (int i = 0; i < dp; i++) rowsL[0][(int64_t)i * S + (v - lo)] = i == p ? (g.oddp[p] ? -1 : 1) : 0;
-                JL[0][v - lo] = v < N ? g.succ[v] : SINK;
+                const int p = v < N ? pidxL[v - lo] : -1;
+                for (int i = 0; i < dp; i++) rowsL[0][(int64_t)i * S + (v - lo)] = i == p ? (oddL[p] ? -1 : 1) : 0;
+                JL[0][v - lo] = v < N ? succL[v - lo] : SINK;
             }
             cl.sync();
             int c = 0;
@@ -361,20 +400,19 @@ __global__ void __launch_bounds__(kSmallThreads) k_solve_cluster(DevGame g, Clus
                 c ^= 1;
                 if (cl_sum(cl, s_part, parity, newly) == 0) break;   // (its cluster barrier publishes the round)
             }
-            cur = c;
-            for (int32_t v = lo + t; v < min(hi, N); v += T) topL[v - lo] = JL[cur][v - lo] != SINK;
-            cl.sync();
+            cur = c;   // (the round's cluster-wide sum already published the final J)
             inner++;
+            if (!has_odd) break;                                      // no Odd vertex: nothing to switch
             int sw = 0;                                               // All_Odd, in place
             for (int32_t v = max(lo, (int32_t)g.n_even) + t; v < min(hi, N); v += T) {
-                const uint32_t e0 = g.rp[v], e1 = g.rp[v + 1];
-                int32_t best = g.col[e0];
+                const uint32_t e0 = rpL[v - lo], e1 = rpL[v - lo + 1];
+                int32_t best = colL[e0];
                 for (uint32_t e = e0 + 1; e < e1; e++) {
-                    const int32_t u = g.col[e];
+                    const int32_t u = colL[e];
                     if (less(cur, u, best)) best = u;
                 }
-                const int32_t cu = g.succ[v];
-                if (best != cu && less(cur, best, cu)) { g.succ[v] = best; sw++; }
+                const int32_t cu = succL[v - lo];
+                if (best != cu && less(cur, best, cu)) { succL[v - lo] = best; sw++; }
             }
             const int nsw = cl_sum(cl, s_part, parity, sw);
             odd_sw += nsw;
@@ -384,21 +422,24 @@ __global__ void __launch_bounds__(kSmallThreads) k_solve_cluster(DevGame g, Clus
         outer++;
         int sw = 0;                                                   // All_Even (sink candidate last)
         for (int32_t v = lo + t; v < min(hi, (int32_t)g.n_even); v += T) {
-            const uint32_t e0 = g.rp[v], e1 = g.rp[v + 1];
-            int32_t best = g.col[e0];
+            const uint32_t e0 = rpL[v - lo], e1 = rpL[v - lo + 1];
+            int32_t best = colL[e0];
             for (uint32_t e = e0 + 1; e < e1; e++) {
-                const int32_t u = g.col[e];
+                const int32_t u = colL[e];
                 if (less(cur, best, u)) best = u;
             }
             if (less(cur, best, SINK)) best = SINK;
-            const int32_t cu = g.succ[v];
-            if (best != cu && less(cur, cu, best)) { g.succ[v] = best; sw++; }
+            const int32_t cu = succL[v - lo];
+            if (best != cu && less(cur, cu, best)) { succL[v - lo] = best; sw++; }
         }
         const int nsw = cl_sum(cl, s_part, parity, sw);
         even_sw += nsw;
         if (nsw == 0) break;
     }
-    for (int32_t v = lo + t; v < min(hi, N); v += T) g.top[v] = topL[v - lo];
+    for (int32_t v = lo + t; v < hiv; v += T) {
+        g.top[v] = JL[cur][v - lo] != SINK;
+        g.succ[v] = succL[v - lo];   // the final profile back to global memory
+    }
     if (r == 0 && t == 0) {
         Ctl *ctl = g.ctl;
         ctl->sm_inner = (unsigned long long)inner;
@@ -411,9 +452,9 @@ __global__ void __launch_bounds__(kSmallThreads) k_solve_cluster(DevGame g, Clus
     cl.sync();   // no CTA leaves while another may still read its shared memory
 }
 
-cudaError_t launch_solve_cluster(const DevGame &g, int C, bool reset, int64_t max_inner, int64_t max_outer,
-                                 cudaStream_t s) {
-    const ClusterLayout L = cluster_layout(g.n_int + 1, g.dp, C);
+cudaError_t launch_solve_cluster(const DevGame &g, int C, int64_t col_cap, bool reset, int64_t max_inner,
+                                 int64_t max_outer, cudaStream_t s) {
+    const ClusterLayout L = cluster_layout(g.n_int + 1, g.dp, C, col_cap);
     cudaError_t e = cudaFuncSetAttribute(k_solve_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
     if (e) return e;
     if (C > 8) {
