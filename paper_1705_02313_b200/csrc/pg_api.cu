@@ -1087,6 +1087,7 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     h->avg_indeg = L.n_int ? (double)L.m_int / (double)L.n_int : 0.0;
     G.n_int = L.n_int;
     G.n_even = L.n_even;
+    G.m_int = L.m_int;
     G.d = L.d;
     G.rp = L.rp; G.col = L.col; G.pidx = L.pidx;
     G.perm = L.perm; G.iperm = L.iperm; G.proj = L.proj;
@@ -1446,7 +1447,7 @@ pg_status pg_solve(pg_game h, uint8_t *winner, int32_t *sigma, int32_t *tau, int
         // fits in shared memory
         const bool small = h->G.n_int + 1 <= h->small_max && !dist_active(h) &&
                            !(h->flags & (PG_BELLMAN_FORD | PG_TRACE)) &&
-                           small_scratch_bytes(h->G.n_int, h->G.dp, check) <= (size_t)h->smem_optin;
+                           small_scratch_bytes(h->G.n_int, h->G.m_int, h->G.dp, check) <= (size_t)h->smem_optin;
         if (small) {
             {
                 PhaseScope ps(h, PH_OTHER);

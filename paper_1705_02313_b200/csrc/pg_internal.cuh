@@ -120,6 +120,7 @@ struct Ctl {
 struct DevGame {
     int64_t n_int;      // internal vertices; SINK = n_int
     int64_t n_even;     // device ids [0, n_even) are Even
+    int64_t m_int;      // internal edges (col entries)
     int32_t d;          // |D|
     int32_t dp;         // padded row width (pow2 <= 128, else multiple of 32)
     int32_t K;          // splitter depth stride
@@ -248,7 +249,7 @@ size_t children_scan_bytes(int64_t n1);
 cudaError_t launch_bf_round(const DevGame &g, int sms, const int32_t *cur, int32_t *nxt,
                             unsigned long long *changed, unsigned long long *rows, cudaStream_t s);
 // whole-solve single-block kernel for small games (pg_small.cu)
-size_t small_scratch_bytes(int64_t n_int, int dp, bool check);
+size_t small_scratch_bytes(int64_t n_int, int64_t m_int, int dp, bool check);
 cudaError_t launch_solve_small(const DevGame &g, bool check, bool reset, int64_t max_inner, int64_t max_outer,
                                cudaStream_t s);
 cudaError_t launch_bf_init(int32_t *rows0, int32_t *rows1, int64_t count, int sms, cudaStream_t s);

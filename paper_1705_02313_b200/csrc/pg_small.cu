@@ -42,10 +42,12 @@ namespace pgsi {
 constexpr int kSmallThreads = 1024;
 
 struct SmallLayout {   // offsets (bytes) inside one scratch region
-    size_t rows[2], J[2], top, M[2], MJ[2], total;
+    size_t rows[2], J[2], top, M[2], MJ[2], rp, col, succ, pidx, oddp, total;
 };
 
-static SmallLayout small_layout(int64_t n1, int dp, bool check) {
+// rows / J / ⊤ of the Wyllie valuation (+ the check mode's max-combine scratch) and the
+// game itself (CSR, profile, priority indices): the loop makes no global load
+static SmallLayout small_layout(int64_t n1, int64_t m, int dp, bool check) {
     SmallLayout L{};
     size_t off = 0;
     auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 15) & ~size_t(15); return o; };
@@ -53,11 +55,18 @@ static SmallLayout small_layout(int64_t n1, int dp, bool check) {
     for (int b = 0; b < 2; b++) L.J[b] = take((size_t)n1 * 4);
     L.top = take((size_t)n1);
     for (int b = 0; b < 2; b++) { L.M[b] = check ? take((size_t)n1 * 4) : 0; L.MJ[b] = check ? take((size_t)n1 * 4) : 0; }
+    L.rp = take((size_t)n1 * 4);
+    L.col = take((size_t)std::max<int64_t>(m, 1) * 4);
+    L.succ = take((size_t)n1 * 4);
+    L.pidx = take((size_t)n1);
+    L.oddp = take((size_t)std::max(dp, 32));
     L.total = off;
     return L;
 }
 
-size_t small_scratch_bytes(int64_t n_int, int dp, bool check) { return small_layout(n_int + 1, dp, check).total; }
+size_t small_scratch_bytes(int64_t n_int, int64_t m_int, int dp, bool check) {
+    return small_layout(n_int + 1, m_int, dp, check).total;
+}
 
 // a ⊏ b on (row, ⊤) pairs; the sink is the finite zero row. Rows are column-major
 // (column i of vertex v at rows[i·n1 + v]) so that the thread-per-vertex loops of a
@@ -87,13 +96,26 @@ __global__ void __launch_bounds__(kSmallThreads) k_solve_small(DevGame g, SmallL
     const int32_t N = (int32_t)g.n_int, SINK = N, n1 = N + 1;
     const int dp = g.dp;
     const int t = threadIdx.x, T = blockDim.x;
+    // the game in shared memory: CSR, profile, priority indices, parity table
+    uint32_t *const rpS = reinterpret_cast<uint32_t *>(base + L.rp);
+    int32_t *const colS = reinterpret_cast<int32_t *>(base + L.col);
+    int32_t *const succS = reinterpret_cast<int32_t *>(base + L.succ);
+    uint8_t *const pidxS = reinterpret_cast<uint8_t *>(base + L.pidx);
+    uint8_t *const oddS = reinterpret_cast<uint8_t *>(base + L.oddp);
+    for (int32_t v = t; v <= N; v += T) {
+        rpS[v] = g.rp[v];
+        if (v < N) { succS[v] = g.succ[v]; pidxS[v] = g.pidx[v]; }
+    }
+    for (uint32_t e = t; e < g.rp[N]; e += T) colS[e] = g.col[e];
+    for (int i = t; i < dp; i += T) oddS[i] = g.oddp[i];
+    __syncthreads();
     int64_t inner = 0, outer = 0, rounds = 0, odd_sw = 0, even_sw = 0;
     int status = 0;   // 0 ok, 1 iteration cap, 2 odd cycle
     int cur = 0;      // buffer holding the final rows / J of the last valuation
     for (;;) {                                                        // Algorithm 1, outer repeat
         if (max_outer > 0 && outer >= max_outer) { status = 1; break; }
         if (reset && outer > 0) {                                     // SI-Reset: τ := τ_init
-            for (int32_t v = (int32_t)g.n_even + t; v < N; v += T) g.succ[v] = g.col[g.rp[v]];
+            for (int32_t v = (int32_t)g.n_even + t; v < N; v += T) succS[v] = colS[rpS[v]];
             __syncthreads();
         }
         bool stop = false;
@@ -101,9 +123,9 @@ __global__ void __launch_bounds__(kSmallThreads) k_solve_small(DevGame g, SmallL
             if (max_inner > 0 && inner >= max_inner) { status = 1; stop = true; break; }
             // ---- valuation: round 0 = (succ, e_pri)
             for (int32_t v = t; v <= N; v += T) {
-                const int p = v < N ? g.pidx[v] : -1;
-                for (int i = 0; i < dp; i++) rows0[(int64_t)i * n1 + v] = i == p ? (g.oddp[p] ? -1 : 1) : 0;
-                J0[v] = v < N ? g.succ[v] : SINK;
+                const int p = v < N ? pidxS[v] : -1;
+                for (int i = 0; i < dp; i++) rows0[(int64_t)i * n1 + v] = i == p ? (oddS[p] ? -1 : 1) : 0;
+                J0[v] = v < N ? succS[v] : SINK;
             }
             __syncthreads();
             int c = 0;
@@ -144,8 +166,8 @@ __global__ void __launch_bounds__(kSmallThreads) k_solve_small(DevGame g, SmallL
                 int32_t *const MJ0 = reinterpret_cast<int32_t *>(base + L.MJ[0]);
                 int32_t *const MJ1 = reinterpret_cast<int32_t *>(base + L.MJ[1]);
                 for (int32_t v = t; v <= N; v += T) {
-                    M0[v] = v < N ? g.pidx[v] : 0;
-                    MJ0[v] = v < N ? g.succ[v] : SINK;
+                    M0[v] = v < N ? pidxS[v] : 0;
+                    MJ0[v] = v < N ? succS[v] : SINK;
                 }
                 __syncthreads();
                 int b = 0;
@@ -163,21 +185,21 @@ __global__ void __launch_bounds__(kSmallThreads) k_solve_small(DevGame g, SmallL
                 const int32_t *Mf = b ? M1 : M0, *MJf = b ? MJ1 : MJ0;
                 int odd = 0;
                 for (int32_t v = t; v < N; v += T)
-                    if (top[v]) odd |= g.oddp[Mf[MJf[v]]];
+                    if (top[v]) odd |= oddS[Mf[MJf[v]]];
                 if (__syncthreads_or(odd)) { status = 2; stop = true; break; }
             }
             // ---- All_Odd (in place: decisions read rows and the vertex's own choice)
             const int32_t *R = cur ? rows1 : rows0;
             int sw = 0;
             for (int32_t v = (int32_t)g.n_even + t; v < N; v += T) {
-                const uint32_t e0 = g.rp[v], e1 = g.rp[v + 1];
-                int32_t best = g.col[e0];
+                const uint32_t e0 = rpS[v], e1 = rpS[v + 1];
+                int32_t best = colS[e0];
                 for (uint32_t e = e0 + 1; e < e1; e++) {
-                    const int32_t u = g.col[e];
+                    const int32_t u = colS[e];
                     if (sm_less(R, top, dp, n1, SINK, u, best)) best = u;
                 }
-                const int32_t cu = g.succ[v];
-                if (best != cu && sm_less(R, top, dp, n1, SINK, best, cu)) { g.succ[v] = best; sw++; }
+                const int32_t cu = succS[v];
+                if (best != cu && sm_less(R, top, dp, n1, SINK, best, cu)) { succS[v] = best; sw++; }
             }
             const int nsw = __syncthreads_count(sw);
             odd_sw += nsw;
@@ -189,21 +211,24 @@ __global__ void __launch_bounds__(kSmallThreads) k_solve_small(DevGame g, SmallL
         const int32_t *R = cur ? rows1 : rows0;
         int sw = 0;
         for (int32_t v = t; v < (int32_t)g.n_even; v += T) {
-            const uint32_t e0 = g.rp[v], e1 = g.rp[v + 1];
-            int32_t best = g.col[e0];
+            const uint32_t e0 = rpS[v], e1 = rpS[v + 1];
+            int32_t best = colS[e0];
             for (uint32_t e = e0 + 1; e < e1; e++) {
-                const int32_t u = g.col[e];
+                const int32_t u = colS[e];
                 if (sm_less(R, top, dp, n1, SINK, best, u)) best = u;
             }
             if (sm_less(R, top, dp, n1, SINK, best, SINK)) best = SINK;
-            const int32_t cu = g.succ[v];
-            if (best != cu && sm_less(R, top, dp, n1, SINK, cu, best)) { g.succ[v] = best; sw++; }
+            const int32_t cu = succS[v];
+            if (best != cu && sm_less(R, top, dp, n1, SINK, cu, best)) { succS[v] = best; sw++; }
         }
         const int nsw = __syncthreads_count(sw);
         even_sw += nsw;
         if (nsw == 0) break;
     }
-    for (int32_t v = t; v < N; v += T) g.top[v] = top[v];
+    for (int32_t v = t; v < N; v += T) {
+        g.top[v] = top[v];
+        g.succ[v] = succS[v];   // the final profile back to global memory
+    }
     if (t == 0) {
         Ctl *ctl = g.ctl;
         ctl->sm_inner = (unsigned long long)inner;
@@ -217,7 +242,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_solve_small(DevGame g, SmallL
 
 cudaError_t launch_solve_small(const DevGame &g, bool check, bool reset, int64_t max_inner, int64_t max_outer,
                                cudaStream_t s) {
-    const SmallLayout L = small_layout(g.n_int + 1, g.dp, check);
+    const SmallLayout L = small_layout(g.n_int + 1, (int64_t)g.m_int, g.dp, check);
     if (L.total > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k_solve_small, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total);
         if (e) return e;
