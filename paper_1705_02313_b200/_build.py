@@ -30,22 +30,26 @@ def nccl_dirs():
     return "/usr/include", "/usr/lib/x86_64-linux-gnu"
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, out: str = LIB, extra=()) -> str:
+    """extra: additional nvcc flags (e.g. -D defines for A/B variants written to `out`)."""
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
     deps = srcs + [os.path.join(CSRC, "pg_internal.cuh"), os.path.join(ROOT, "include", "pg.h")]
-    if not force and os.path.exists(LIB):
-        t = os.path.getmtime(LIB)
+    if not force and os.path.exists(out):
+        t = os.path.getmtime(out)
         if all(os.path.getmtime(d) <= t for d in deps):
             return LIB
     ninc, nlib = nccl_dirs()
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
            "-Xptxas", "-v" if verbose else "-O3", "-I", os.path.join(ROOT, "include"), "-I", ninc,
-           "-o", LIB + ".tmp", *srcs, "-L", nlib, "-l:libnccl.so.2", "-Xlinker", f"-rpath={nlib}"]
+           *extra, "-o", out + ".tmp", *srcs, "-L", nlib, "-l:libnccl.so.2", "-Xlinker", f"-rpath={nlib}"]
     subprocess.check_call(cmd)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(out + ".tmp", out)
+    return out
 
 
 if __name__ == "__main__":
+    # python _build.py [-v] [-o OUT.so] [-DNAME=VAL ...]
     import sys
-    print(build(force=True, verbose="-v" in sys.argv))
+    a = sys.argv[1:]
+    out = a[a.index("-o") + 1] if "-o" in a else LIB
+    print(build(force=True, verbose="-v" in a, out=os.path.abspath(out), extra=[x for x in a if x.startswith("-D")]))

@@ -436,16 +436,24 @@ __global__ void __launch_bounds__(kThreads) k_v2_rows(DevGame g, int nchunk) {
 // prefix of the vertex x the walk ended at (x = sink: the empty exact prefix)
 // and store the result as v's compact prefix. Exact by the one-unit insert rule
 // (DESIGN.md "Compact prefix"); clears the touched histogram bytes.
+__device__ __forceinline__ void cpx_merge_store_b(const DevGame &g, int64_t v, uint8_t *hb, uint32_t mask,
+                                                  const uint32_t (&b)[8], uint32_t *ow);
 __device__ __forceinline__ void cpx_merge_store(const DevGame &g, int64_t v, uint8_t *hb, uint32_t mask,
                                                 int32_t x, uint32_t *ow) {
-    const int maxp = g.cpx_pairs;
-    const uint32_t mask0 = mask;
     uint32_t b[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     if (x != (int32_t)g.n_int) {
         const uint4 *cpx4 = reinterpret_cast<const uint4 *>(g.cpx);
         const uint4 b0 = __ldcg(cpx4 + 2 * (int64_t)x), b1 = __ldcg(cpx4 + 2 * (int64_t)x + 1);
         b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w; b[4] = b1.x; b[5] = b1.y; b[6] = b1.z; b[7] = b1.w;
     }
+    cpx_merge_store_b(g, v, hb, mask, b, ow);
+}
+
+// The same with the base prefix already loaded (b = 0: the sink's empty prefix).
+__device__ __forceinline__ void cpx_merge_store_b(const DevGame &g, int64_t v, uint8_t *hb, uint32_t mask,
+                                                  const uint32_t (&b)[8], uint32_t *ow) {
+    const int maxp = g.cpx_pairs;
+    const uint32_t mask0 = mask;
     const int nb = (int)((b[0] >> 2) & 7u);
     const bool tb = (b[0] & 2u) != 0;
     int np = 0, j = 1;
@@ -1019,7 +1027,7 @@ __device__ __forceinline__ int cmp_pref(const DevGame &g, const uint4 *cpx, int3
 template <bool ODD, bool HARD>
 __device__ __forceinline__ int switch_vertex(const DevGame &g, int64_t v, const uint4 *cpx,
                                              unsigned long long &reads, unsigned long long &fulls,
-                                             unsigned long long &pref) {
+                                             unsigned long long &pref, int32_t &best_out) {
     constexpr int B = 6;   // one batch for out-degree <= 5 plus the sink (measured: 4 -> 6 saves 1.1 ms per config-3 solve)
     const int32_t SINK = (int32_t)g.n_int;
     const int32_t cur = __ldcg(g.succ + v);
@@ -1074,10 +1082,25 @@ __device__ __forceinline__ int switch_vertex(const DevGame &g, int64_t v, const 
     if (ODD ? r < 0 : r > 0) {
         // σ[S] / τ[S] is applied after both passes (k_apply_switches): the hard pass
         // re-walks plays of the *current* profile, so succ must not change before it.
-        g.swl[atomicAdd(&g.ctl->nswl, 1ull)] = make_int2((int32_t)v, best);
+        // The caller appends (v, best) to the switch list (append_switch).
+        best_out = best;
         return 1;
     }
     return 0;
+}
+
+// Append (v, best) to the switch list when sw: one atomic per warp (the lanes still in
+// the caller's loop), not one per switch: a full All_Odd / All_Even switches up to
+// millions of vertices, and same-address atomics serialise in L2.
+__device__ __forceinline__ void append_switch(const DevGame &g, bool sw, int64_t v, int32_t best) {
+    const unsigned am = __activemask();
+    const unsigned m = __ballot_sync(am, sw);
+    if (!m) return;
+    const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+    unsigned long long b = 0;
+    if (lane == leader) b = atomicAdd(&g.ctl->nswl, (unsigned long long)__popc(m));
+    b = __shfl_sync(am, b, leader);
+    if (sw) g.swl[b + __popc(m & ((1u << lane) - 1u))] = make_int2((int32_t)v, best);
 }
 
 __global__ void k_apply_switches(DevGame g, int force) {
@@ -1104,7 +1127,9 @@ __global__ void __launch_bounds__(kThreads) k_switch(DevGame g, const int32_t *v
          i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t v = HARD ? (int64_t)__ldcg(g.hard + i) : (lst ? (int64_t)__ldcg(vlist + i) : i);
         if (lst && g.sharded && !sh_owns(g, v)) continue;   // another rank's vertex
-        const int r = switch_vertex<ODD, HARD>(g, v, cpx, reads, fulls, pref);
+        int32_t best = -1;
+        const int r = switch_vertex<ODD, HARD>(g, v, cpx, reads, fulls, pref, best);
+        append_switch(g, r == 1, v, best);
         if (r == 1) nsw++;
         if constexpr (!HARD) {
             if (r == 2) g.hard[atomicAdd(&g.ctl->nhard, 1ull)] = (int32_t)v;
@@ -1316,8 +1341,14 @@ __device__ __forceinline__ void trace_level(const DevGame &g, int64_t width, int
 // beyond it go to a global overflow list (and the D list) and are the roots of the
 // next phase, which every block shares again after one grid barrier. New D vertices
 // are staged in shared memory and flushed to the D list with one atomic per block.
-constexpr int kCloCap = 2048;      // block frontier capacity (vertices)
-constexpr int kCloStage = 4096;    // D-list staging capacity (vertices)
+#ifndef PGSI_CLO_EB
+#define PGSI_CLO_EB 4
+#endif
+#ifndef PGSI_CLO_CAP
+#define PGSI_CLO_CAP 2048
+#endif
+constexpr int kCloCap = PGSI_CLO_CAP;                       // block frontier capacity (vertices)
+constexpr int kCloStage = 4096;                             // D-list staging capacity (vertices)
 constexpr size_t kCloSmem = (size_t)(2 * kCloCap + kCloStage) * (sizeof(int32_t) + sizeof(uint2));
 
 // Expand the roots (Rv, Rr)[lo, hi) of this block; returns false if the level cap hit.
@@ -1368,7 +1399,7 @@ __device__ bool closure_block(const DevGame &g, const int32_t *Rv, const uint2 *
                 // offsets, and issues all loads of the round together: a round is two
                 // dependent loads however uneven the degrees (a lane-per-vertex loop
                 // costs two per 8 edges of the warp's largest degree).
-                constexpr int EB = 4;
+                constexpr int EB = PGSI_CLO_EB;
                 const uint32_t deg = f >= 0 ? re - rb : 0u;
                 uint32_t incl_d = deg;
 #pragma unroll
@@ -1519,43 +1550,57 @@ __device__ __forceinline__ void inc_v2_item(const DevGame &g, int64_t i, int64_t
     const int32_t v = i < nd ? __ldcg(g.Dl + i) : -1;
     uint2 rr = make_uint2(0u, 0u);
     if (e_in_v2 && v >= 0) rr = __ldcg(g.Dr + i);
+    // Every load that depends on v alone is issued together: v is in D, so its first
+    // walk step needs no mark check; each later step loads the mark, the priority and
+    // the successor of x in one round trip (the last step's two are not used).
+    const int32_t vs = v >= 0 ? v : 0;
+    uint32_t cm = 0;
+    unsigned long long e0 = 0;
+    if (odd_s) cm = __ldcg(g.cmark + vs);
+    else e0 = __ldcg(jl + vs);
+    const uint32_t p0 = __ldg(g.pidx + vs);
+    int32_t x = __ldcg(g.succ + vs);
     if (odd_s) {
-        const bool addc = v >= 0 && __ldcg(g.cmark + v) != cepoch;
+        const bool addc = v >= 0 && cm != cepoch;
         if (addc) g.cmark[v] = cepoch;
         warp_append(addc, v, g.Cl, &ctl->nC);
     }
     if (v >= 0) {
-        bool fin = true;
-        if (!odd_s) {
-            const unsigned long long e = __ldcg(jl + v);
-            fin = (uint32_t)e == SINK;
-        }
+        const bool fin = odd_s || (uint32_t)e0 == SINK;
         g.top[v] = fin ? 0 : 1;
         if (!fin) {
             put_cpx(g, v, make_uint4(1u, 0, 0, 0), make_uint4(0, 0, 0, 0));
         } else {
-            uint32_t mask = 0, steps = 0;
-            int32_t x = v;
-            while (x != (int32_t)N && __ldcg(g.dmark + x) == ep) {
+            uint32_t mask = 1u << p0, steps = 1;
+            hb[p0] = 1;
+            while (x != (int32_t)N) {
+                const uint32_t dm = __ldcg(g.dmark + x);
                 const uint32_t p = __ldg(g.pidx + x);
-                x = __ldcg(g.succ + x);
+                const int32_t nx = __ldcg(g.succ + x);
+                if (dm != ep) break;
                 if (++hb[p] == 255) { atomicOr(&ctl->inc_overflow, 1ull); break; }
                 mask |= 1u << p;
                 steps++;
+                x = nx;
             }
             wsteps += steps;
+            // the exit x is clean (final prefix, final jl) or the sink: both loads at once
+            uint32_t bw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            unsigned long long ex = pack_jl(SINK, 0u);
+            if (x != (int32_t)N) {
+                const uint4 *cpx4 = reinterpret_cast<const uint4 *>(g.cpx);
+                const uint4 b0 = __ldcg(cpx4 + 2 * (int64_t)x), b1 = __ldcg(cpx4 + 2 * (int64_t)x + 1);
+                if (odd_s) ex = __ldcg(jl + x);
+                bw[0] = b0.x; bw[1] = b0.y; bw[2] = b0.z; bw[3] = b0.w;
+                bw[4] = b1.x; bw[5] = b1.y; bw[6] = b1.z; bw[7] = b1.w;
+            }
             if (odd_s) {   // depth(v) = steps + depth(x); x is clean (final jl) or the sink
-                uint32_t dx = 0;
-                if (x != (int32_t)N) {
-                    const unsigned long long ex = __ldcg(jl + x);
-                    if ((uint32_t)ex != SINK) atomicOr(&ctl->inc_overflow, 1ull);   // clean ⊤ exit: redo in full
-                    dx = (uint32_t)(ex >> 32);
-                }
-                uint32_t dv = steps + dx;
+                if ((uint32_t)ex != SINK) atomicOr(&ctl->inc_overflow, 1ull);   // clean ⊤ exit: redo in full
+                uint32_t dv = steps + (uint32_t)(ex >> 32);
                 if (dv > 0x7fffffffu) dv = 0x7fffffffu;
                 jl[v] = pack_jl(SINK, dv);
             }
-            cpx_merge_store(g, v, hb, mask, x, ow);
+            cpx_merge_store_b(g, v, hb, mask, bw, ow);
         }
     }
     if (e_in_v2) expand_rev<1>(g, -1, rr.x, rr.y, g.emark, ep, g.El, &ctl->nE);
@@ -1843,7 +1888,9 @@ __global__ void __launch_bounds__(kIncThreads) k_inc_iter(DevGame g) {
         for (int64_t i = tid; i < ne; i += stride) {
             const int64_t v = __ldcg(g.El + i);
             if (g.sharded && !sh_owns(g, v)) continue;   // another rank's vertex
-            const int rr = switch_vertex<true, false>(g, v, cpx, reads, fulls, pref);
+            int32_t best = -1;
+            const int rr = switch_vertex<true, false>(g, v, cpx, reads, fulls, pref, best);
+            append_switch(g, rr == 1, v, best);
             if (rr == 1) nsw++;
             else if (rr == 2) g.hard[atomicAdd(&ctl->nhard, 1ull)] = (int32_t)v;
         }
@@ -1854,7 +1901,10 @@ __global__ void __launch_bounds__(kIncThreads) k_inc_iter(DevGame g) {
         const int64_t nh = (int64_t)bcast_ld(&ctl->nhard);
         for (int64_t i = tid; i < nh; i += stride) {
             const int64_t v = __ldcg(g.hard + i);
-            if (switch_vertex<true, true>(g, v, cpx, reads, fulls, pref) == 1) nsw++;
+            int32_t best = -1;
+            const int rr = switch_vertex<true, true>(g, v, cpx, reads, fulls, pref, best);
+            append_switch(g, rr == 1, v, best);
+            if (rr == 1) nsw++;
         }
     }
     gbar(ctl);
@@ -1937,14 +1987,18 @@ __global__ void __launch_bounds__(kIncThreads) k_inc_iter(DevGame g) {
     unsigned long long ereads = 0, efulls = 0, epref = 0;
     for (int64_t i = tid; i < nee; i += stride) {
         const int64_t v = __ldcg(g.El + i);
-        if (switch_vertex<false, false>(g, v, cpx, ereads, efulls, epref) == 2)
-            g.hard[atomicAdd(&ctl->nhard, 1ull)] = (int32_t)v;
+        int32_t best = -1;
+        const int rr = switch_vertex<false, false>(g, v, cpx, ereads, efulls, epref, best);
+        append_switch(g, rr == 1, v, best);
+        if (rr == 2) g.hard[atomicAdd(&ctl->nhard, 1ull)] = (int32_t)v;
     }
     gbar(ctl);
     const int64_t nhe = (int64_t)bcast_ld(&ctl->nhard);
     for (int64_t i = tid; i < nhe; i += stride) {
         const int64_t v = __ldcg(g.hard + i);
-        switch_vertex<false, true>(g, v, cpx, ereads, efulls, epref);
+        int32_t best = -1;
+        const int rr = switch_vertex<false, true>(g, v, cpx, ereads, efulls, epref, best);
+        append_switch(g, rr == 1, v, best);
     }
     gbar(ctl);
     const int64_t nes = (int64_t)bcast_ld(&ctl->nswl);   // σ := σ[All_Even]; it is S of the next step
@@ -2004,8 +2058,10 @@ __global__ void __launch_bounds__(kThreads) k_inc_v2_split(DevGame g) {
     const int64_t wbase = blockIdx.x * (int64_t)blockDim.x + threadIdx.x - lane;
     for (int64_t b0 = wbase; b0 < nd; b0 += (int64_t)gridDim.x * blockDim.x)
         inc_v2_item(g, b0 + lane, nd, ep, cepoch, odd_s, e_in_v2, hb, ow, wsteps);
-    wsteps = block_sum(wsteps);
-    if (threadIdx.x == 0 && wsteps) atomicAdd(&ctl->walk_steps, wsteps);
+    // a warp sum, not a block sum: no block waits for its slowest warp's walks
+    // (ncu: 26 % of the stall samples sat at block_sum's barrier)
+    for (int o = 16; o; o >>= 1) wsteps += __shfl_xor_sync(FULL, wsteps, o);
+    if (lane == 0 && wsteps) atomicAdd(&ctl->walk_steps, wsteps);
 }
 
 __global__ void k_inc_split_fin(Ctl *ctl) {
