@@ -527,6 +527,7 @@ pg_status valuate_and_switch(pg_game h, bool odd, bool want_cdom, bool do_switch
     }
     const double t_start = h->trace ? now_ms() : 0.0;
     int64_t done_inc = 0;      // inner iterations completed by an incremental launch that then aborted
+    bool was_split = false;    // the last incremental step continued in launch_inc_split
     for (;;) {
         pg_status rc = valuate_dev(h, want_cdom, !do_switch, inc, bfs, max_steps);
         if (rc) return rc;
@@ -537,6 +538,7 @@ pg_status valuate_and_switch(pg_game h, bool odd, bool want_cdom, bool do_switch
         }
         rc = readback(h);
         if (rc) return rc;
+        was_split = inc && h->h_ctl->split;
         if (inc && h->h_ctl->split) {   // a big step: V2 / E / All_Odd continue at full occupancy
             {
                 PhaseScope ps(h, PH_INC);
@@ -600,7 +602,11 @@ pg_status valuate_and_switch(pg_game h, bool odd, bool want_cdom, bool do_switch
         fprintf(stderr, "\n");
         CK(h, cudaMemset(h->G.lvlog, 0, 8));
     }
-    if (h->trace && inc && h->G.trace_ts) {
+    if (h->trace && inc && h->G.trace_ts && was_split) {   // V2 / E / All_Odd ran in launch_inc_split
+        const unsigned long long *t = h->h_ctl->ts;
+        fprintf(stderr, "[pgsi]   inc phases (us): closure %.1f  (big step: V1 on D, V2, E and All_Odd in the split kernels)\n",
+                (t[1] - t[0]) * 1e-3);
+    } else if (h->trace && inc && h->G.trace_ts) {
         const unsigned long long *t = h->h_ctl->ts;
         fprintf(stderr, "[pgsi]   inc phases (us): closure %.1f  C %.1f  V1 %.1f  V2 %.1f  E %.1f  switch %.1f  hard %.1f  apply %.1f\n",
                 (t[1] - t[0]) * 1e-3, (t[2] - t[1]) * 1e-3, (t[3] - t[2]) * 1e-3, (t[4] - t[3]) * 1e-3,
