@@ -58,6 +58,7 @@ struct Ctl {
     unsigned long long inc_overflow;// incremental V2 walk too long for byte counts -> redo in full
     unsigned long long dlevels;     // BFS levels of the dirty closure
     unsigned long long dcnt[3];     // per-level append counters of the dirty BFS (rotating)
+    unsigned long long dcnt_p[2][3];// k_inc_iter: the same per phase / level, one set per step parity
     unsigned long long bfs_abort;   // top-down BFS valuation exceeded bfs_max_levels
     unsigned long long steps_done;  // incremental launch: inner iterations completed on the device
     unsigned long long last_sw;     // ... switches of the last completed one (0 = converged)

@@ -74,6 +74,28 @@ __device__ __forceinline__ T block_sum(T x) {
     return s;  // valid in thread 0
 }
 
+// N block sums with one pair of barriers (valid in thread 0)
+template <int N>
+__device__ __forceinline__ void block_sum_n(unsigned long long (&x)[N]) {
+    __shared__ unsigned long long red[32][N];
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+#pragma unroll
+    for (int k = 0; k < N; k++)
+        for (int o = 16; o; o >>= 1) x[k] += __shfl_xor_sync(FULL, x[k], o);
+    __syncthreads();
+    if (l == 0)
+#pragma unroll
+        for (int k = 0; k < N; k++) red[w][k] = x[k];
+    __syncthreads();
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int k = 0; k < N; k++) {
+            unsigned long long s = 0;
+            for (int i = 0; i < (int)(blockDim.x >> 5); i++) s += red[i][k];
+            x[k] = s;
+        }
+}
+
 template <typename T>
 __device__ __forceinline__ T block_max(T x) {
     __shared__ T red[32];
@@ -1639,6 +1661,8 @@ __global__ void __launch_bounds__(kIncThreads) k_inc_iter(DevGame g) {
     bool s_from_odd = __ldcg(&ctl->lp_s_odd) != 0;   // this step's S came from All_Odd
     for (int step = 0;; step++) {
     const uint32_t ep = epoch0 + (uint32_t)step * (even_in ? 2u : 1u);
+    // this step's closure counters; the other parity's set is zeroed below for the next step
+    unsigned long long *DC = ctl->dcnt_p[step & 1];
     if (blockIdx.x == 0 && threadIdx.x == 0) ctl->steps_done = (unsigned long long)step;
     trace_ts(g, 0);
     // ---- 1. dirty closure
@@ -1651,7 +1675,14 @@ __global__ void __launch_bounds__(kIncThreads) k_inc_iter(DevGame g) {
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) ctl->nDl = (unsigned long long)ns;
     gbar(ctl);
-    if (blockIdx.x == 0 && threadIdx.x == 0) { ctl->nswl = 0; ctl->nhard = 0; ctl->nE = 0; }  // steps 4-5 append anew
+    if (blockIdx.x == 0 && threadIdx.x == 0) {   // steps 4-5 append anew; the next step's counters
+        ctl->nswl = 0;                             // (nobody uses them before this step's end)
+        ctl->nhard = 0;
+        ctl->nE = 0;
+        ctl->step_sw[(step + 1) & 1] = 0;
+        unsigned long long *dn = ctl->dcnt_p[(step + 1) & 1];
+        dn[0] = dn[1] = dn[2] = 0;
+    }
     int64_t lo = 0, hi = ns;
     int levels = 0;
     if (g.inc_closure == 1) {
@@ -1661,7 +1692,7 @@ __global__ void __launch_bounds__(kIncThreads) k_inc_iter(DevGame g) {
         const uint2 *Rr = g.Dr;
         int64_t nr = ns;
         for (;;) {
-            unsigned long long *ocnt = &ctl->dcnt[phase % 3];   // reset two phases ahead
+            unsigned long long *ocnt = &DC[phase % 3];   // reset two phases ahead
             int32_t *Ov = g.Ol[phase & 1];
             uint2 *Or = g.Or[phase & 1];
             const int64_t per = (nr + gridDim.x - 1) / gridDim.x;
@@ -1672,7 +1703,7 @@ __global__ void __launch_bounds__(kIncThreads) k_inc_iter(DevGame g) {
             nr = (int64_t)bcast_ld(ocnt);
             hi = (int64_t)bcast_ld(&ctl->nDl);
             const bool abort = bcast_ld(&ctl->inc_overflow) != 0 || hi > g.inc_max_dirty;
-            if (blockIdx.x == 0 && threadIdx.x == 0) ctl->dcnt[(phase + 2) % 3] = 0;
+            if (blockIdx.x == 0 && threadIdx.x == 0) DC[(phase + 2) % 3] = 0;
             if (threadIdx.x == 0) atomicMax(&ctl->dlevels, (unsigned long long)maxlev);
             if (abort) {
                 // deep or huge closure: a from-scratch valuation is cheaper. Nothing but
@@ -1746,7 +1777,7 @@ __global__ void __launch_bounds__(kIncThreads) k_inc_iter(DevGame g) {
         }
         levels++;
         glev++;
-        unsigned long long *cnt = &ctl->dcnt[glev % 3];     // reset two grid levels ahead: no
+        unsigned long long *cnt = &DC[glev % 3];     // reset two grid levels ahead: no
         int32_t *out = g.Dl + hi;                           // block reads a count still being written
         for (int64_t b0 = lo + wbase; b0 < hi; b0 += stride) {
             const int64_t i = b0 + lane;
@@ -1760,7 +1791,7 @@ __global__ void __launch_bounds__(kIncThreads) k_inc_iter(DevGame g) {
         }
         gbar(ctl);
         const int64_t added = (int64_t)bcast_ld(cnt);
-        if (blockIdx.x == 0 && threadIdx.x == 0) ctl->dcnt[(glev + 2) % 3] = 0;
+        if (blockIdx.x == 0 && threadIdx.x == 0) DC[(glev + 2) % 3] = 0;
         lo = hi;
         hi += added;
         if (blockIdx.x == 0 && threadIdx.x == 0) trace_level(g, added, levels, false);
@@ -1903,36 +1934,33 @@ __global__ void __launch_bounds__(kIncThreads) k_inc_iter(DevGame g) {
     }
     gbar(ctl);
     trace_ts(g, 6);
-    if (!ovf) {
-        const int64_t nh = (int64_t)bcast_ld(&ctl->nhard);
-        for (int64_t i = tid; i < nh; i += stride) {
-            const int64_t v = __ldcg(g.hard + i);
-            int32_t best = -1;
-            const int rr = switch_vertex<true, true>(g, v, cpx, reads, fulls, pref, best);
-            append_switch(g, rr == 1, v, best);
-            if (rr == 1) nsw++;
-        }
+    const int64_t nh = ovf ? 0 : (int64_t)bcast_ld(&ctl->nhard);
+    for (int64_t i = tid; i < nh; i += stride) {
+        const int64_t v = __ldcg(g.hard + i);
+        int32_t best = -1;
+        const int rr = switch_vertex<true, true>(g, v, cpx, reads, fulls, pref, best);
+        append_switch(g, rr == 1, v, best);
+        if (rr == 1) nsw++;
     }
-    gbar(ctl);
+    if (nh > 0) gbar(ctl);   // (no hard vertex: the switch list is final since the last barrier)
     trace_ts(g, 7);
     const int64_t nsl = g.sharded ? 0 : (int64_t)bcast_ld(&ctl->nswl);
     for (int64_t i = tid; i < nsl; i += stride) {   // sharded: applied after the exchange
         const int2 e = __ldcg(g.swl + i);
         g.succ[e.x] = e.y;
     }
-    unsigned long long t = block_sum(nsw);
-    if (threadIdx.x == 0 && t) {
-        atomicAdd(&ctl->odd_switches, t);
-        atomicAdd(&ctl->step_sw[step & 1], t);
+    unsigned long long sums[5] = {nsw, reads, fulls, pref, wsteps};
+    block_sum_n<5>(sums);
+    if (threadIdx.x == 0) {
+        if (sums[0]) {
+            atomicAdd(&ctl->odd_switches, sums[0]);
+            atomicAdd(&ctl->step_sw[step & 1], sums[0]);
+        }
+        if (sums[1]) atomicAdd(&ctl->rows_odd, sums[1]);
+        if (sums[2]) atomicAdd(&ctl->full_odd, sums[2]);
+        if (sums[3]) atomicAdd(&ctl->cpx_gathers, sums[3]);
+        if (sums[4]) atomicAdd(&ctl->walk_steps, sums[4]);
     }
-    t = block_sum(reads);
-    if (threadIdx.x == 0 && t) atomicAdd(&ctl->rows_odd, t);
-    t = block_sum(fulls);
-    if (threadIdx.x == 0 && t) atomicAdd(&ctl->full_odd, t);
-    t = block_sum(pref);
-    if (threadIdx.x == 0 && t) atomicAdd(&ctl->cpx_gathers, t);
-    t = block_sum(wsteps);
-    if (threadIdx.x == 0 && t) atomicAdd(&ctl->walk_steps, t);
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         ctl->nD = (unsigned long long)nd;
         ctl->dlevels = (unsigned long long)levels;
@@ -1951,10 +1979,7 @@ __global__ void __launch_bounds__(kIncThreads) k_inc_iter(DevGame g) {
         ctl->last_sw = sw;
         ctl->nD_sum += (unsigned long long)nd;
         ctl->nE_sum += (unsigned long long)ne;
-        ctl->step_sw[(step + 1) & 1] = 0;
-        ctl->dcnt[0] = ctl->dcnt[1] = ctl->dcnt[2] = 0;
-        ctl->newfin[0] = ctl->newfin[1] = ctl->newfin[2] = 0;
-        ctl->nE = 0;
+        ctl->newfin[0] = ctl->newfin[1] = ctl->newfin[2] = 0;   // read by no one until the next step's V1
     }
     if (sw != 0) {
         s_from_odd = true;
@@ -1964,8 +1989,7 @@ __global__ void __launch_bounds__(kIncThreads) k_inc_iter(DevGame g) {
             if (blockIdx.x == 0 && threadIdx.x == 0) ctl->end_kind = 0;
             return;
         }
-        gbar(ctl);   // the resets above precede the next step's appends
-        continue;
+        continue;    // (the next step's counters were zeroed at this step's start, its S is final: no barrier)
     }
     // ---- 9. S_Odd = ∅: the best response is final. All_Even over C here (
     // the same kernels' logic as launch_even_inc) when allowed, else back to the caller.
@@ -2006,18 +2030,19 @@ __global__ void __launch_bounds__(kIncThreads) k_inc_iter(DevGame g) {
         const int rr = switch_vertex<false, true>(g, v, cpx, ereads, efulls, epref, best);
         append_switch(g, rr == 1, v, best);
     }
-    gbar(ctl);
+    if (nhe > 0) gbar(ctl);
     const int64_t nes = (int64_t)bcast_ld(&ctl->nswl);   // σ := σ[All_Even]; it is S of the next step
     for (int64_t i = tid; i < nes; i += stride) {
         const int2 e = __ldcg(g.swl + i);
         g.succ[e.x] = e.y;
     }
-    t = block_sum(ereads);
-    if (threadIdx.x == 0 && t) atomicAdd(&ctl->rows_even, t);
-    t = block_sum(epref);
-    if (threadIdx.x == 0 && t) atomicAdd(&ctl->cpx_gathers, t);
-    t = block_sum(efulls);
-    if (threadIdx.x == 0 && t) atomicAdd(&ctl->full_even, t);
+    unsigned long long esums[3] = {ereads, epref, efulls};
+    block_sum_n<3>(esums);
+    if (threadIdx.x == 0) {
+        if (esums[0]) atomicAdd(&ctl->rows_even, esums[0]);
+        if (esums[1]) atomicAdd(&ctl->cpx_gathers, esums[1]);
+        if (esums[2]) atomicAdd(&ctl->full_even, esums[2]);
+    }
     gbar(ctl);   // the even list is applied before the next step's closure reads succ
     cepoch++;    // a new C starts: changes after this All_Even
     c_valid = true;
