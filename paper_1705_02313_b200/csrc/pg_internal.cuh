@@ -62,7 +62,6 @@ struct Ctl {
     unsigned long long bfs_abort;   // top-down BFS valuation exceeded bfs_max_levels
     unsigned long long steps_done;  // incremental launch: inner iterations completed on the device
     unsigned long long last_sw;     // ... switches of the last completed one (0 = converged)
-    unsigned long long step_sw[2];  // ... per-step switch counts (alternating)
     unsigned long long nD_sum;      // ... |D| summed over its steps
     unsigned long long nE_sum;      // ... |E| summed over its steps
     unsigned long long cpx_gathers; // switch steps: 32 B prefix gathers after an undecided key compare

@@ -1675,11 +1675,10 @@ __global__ void __launch_bounds__(kIncThreads) k_inc_iter(DevGame g) {
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) ctl->nDl = (unsigned long long)ns;
     gbar(ctl);
-    if (blockIdx.x == 0 && threadIdx.x == 0) {   // steps 4-5 append anew; the next step's counters
-        ctl->nswl = 0;                             // (nobody uses them before this step's end)
+    if (blockIdx.x == 0 && threadIdx.x == 0) {   // steps 4-5 append anew; the next step's closure
+        ctl->nswl = 0;                             // counters (nobody uses them before this step's end)
         ctl->nhard = 0;
         ctl->nE = 0;
-        ctl->step_sw[(step + 1) & 1] = 0;
         unsigned long long *dn = ctl->dcnt_p[(step + 1) & 1];
         dn[0] = dn[1] = dn[2] = 0;
     }
@@ -1944,7 +1943,9 @@ __global__ void __launch_bounds__(kIncThreads) k_inc_iter(DevGame g) {
     }
     if (nh > 0) gbar(ctl);   // (no hard vertex: the switch list is final since the last barrier)
     trace_ts(g, 7);
-    const int64_t nsl = g.sharded ? 0 : (int64_t)bcast_ld(&ctl->nswl);
+    // the switch list is final here: its length is this step's switch count (the loop test)
+    const int64_t nsn = (int64_t)bcast_ld(&ctl->nswl);
+    const int64_t nsl = g.sharded ? 0 : nsn;
     for (int64_t i = tid; i < nsl; i += stride) {   // sharded: applied after the exchange
         const int2 e = __ldcg(g.swl + i);
         g.succ[e.x] = e.y;
@@ -1952,10 +1953,7 @@ __global__ void __launch_bounds__(kIncThreads) k_inc_iter(DevGame g) {
     unsigned long long sums[5] = {nsw, reads, fulls, pref, wsteps};
     block_sum_n<5>(sums);
     if (threadIdx.x == 0) {
-        if (sums[0]) {
-            atomicAdd(&ctl->odd_switches, sums[0]);
-            atomicAdd(&ctl->step_sw[step & 1], sums[0]);
-        }
+        if (sums[0]) atomicAdd(&ctl->odd_switches, sums[0]);
         if (sums[1]) atomicAdd(&ctl->rows_odd, sums[1]);
         if (sums[2]) atomicAdd(&ctl->full_odd, sums[2]);
         if (sums[3]) atomicAdd(&ctl->cpx_gathers, sums[3]);
@@ -1970,10 +1968,10 @@ __global__ void __launch_bounds__(kIncThreads) k_inc_iter(DevGame g) {
     if (ovf) return;   // walk overflow: nothing switched; the host redoes this step in full
 
     // ---- 8. next inner iteration on the device while it stays incremental:
-    // S = this step's switch list (nswl), applied above
-    gbar(ctl);
-    const unsigned long long sw = bcast_ld(&ctl->step_sw[step & 1]);
-    const int64_t nsn = (int64_t)bcast_ld(&ctl->nswl);
+    // S = this step's switch list (nswl), applied above. No barrier: the next step's
+    // closure reads succ only after its first barrier, and nothing written before that
+    // barrier is read by this step's apply.
+    const unsigned long long sw = (unsigned long long)nsn;
     if (blockIdx.x == 0 && threadIdx.x == 0) {   // every reader of these is behind a barrier
         ctl->steps_done = (unsigned long long)step + 1;
         ctl->last_sw = sw;
@@ -2054,7 +2052,6 @@ __global__ void __launch_bounds__(kIncThreads) k_inc_iter(DevGame g) {
         ctl->nc_in += (unsigned long long)nc;
         ctl->nC = 0;
         ctl->lp_cepoch_out = cepoch;
-        ctl->step_sw[(step + 1) & 1] = 0;
         ctl->end_kind = nes == 0 ? 3 : 2;
     }
     if (nes == 0) return;   // S_Even = ∅: σ is optimal; the solve is done
