@@ -60,6 +60,24 @@ __device__ __forceinline__ unsigned long long bcast_ld(const unsigned long long 
     return s;
 }
 
+// N grid-wide counters read right after a grid barrier: thread 0 issues the N loads
+// together (one round trip) and broadcasts them through shared memory.
+template <int N>
+__device__ __forceinline__ void bcast_ld_n(const unsigned long long *const (&p)[N], unsigned long long (&out)[N]) {
+    __shared__ unsigned long long s[N];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long v[N];
+#pragma unroll
+        for (int k = 0; k < N; k++) v[k] = __ldcg(p[k]);
+#pragma unroll
+        for (int k = 0; k < N; k++) s[k] = v[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < N; k++) out[k] = s[k];
+}
+
 template <typename T>
 __device__ __forceinline__ T block_sum(T x) {
     __shared__ T red[32];
@@ -1698,12 +1716,14 @@ __global__ void __launch_bounds__(kIncThreads) k_inc_iter(DevGame g) {
             const int64_t blo = min(nr, (int64_t)blockIdx.x * per), bhi = min(nr, blo + per);
             if (!closure_block(g, Rv, Rr, blo, bhi, ep, Ov, Or, ocnt, maxlev) && threadIdx.x == 0)
                 atomicOr(&ctl->inc_overflow, 1ull);
-            gbar(ctl);
-            nr = (int64_t)bcast_ld(ocnt);
-            hi = (int64_t)bcast_ld(&ctl->nDl);
-            const bool abort = bcast_ld(&ctl->inc_overflow) != 0 || hi > g.inc_max_dirty;
-            if (blockIdx.x == 0 && threadIdx.x == 0) DC[(phase + 2) % 3] = 0;
             if (threadIdx.x == 0) atomicMax(&ctl->dlevels, (unsigned long long)maxlev);
+            gbar(ctl);
+            unsigned long long cv[3];
+            bcast_ld_n<3>({ocnt, &ctl->nDl, &ctl->inc_overflow}, cv);
+            nr = (int64_t)cv[0];
+            hi = (int64_t)cv[1];
+            const bool abort = cv[2] != 0 || hi > g.inc_max_dirty;
+            if (blockIdx.x == 0 && threadIdx.x == 0) DC[(phase + 2) % 3] = 0;
             if (abort) {
                 // deep or huge closure: a from-scratch valuation is cheaper. Nothing but
                 // marks (epoch-scoped) has been written; the host redoes the step in full.
@@ -1913,8 +1933,10 @@ __global__ void __launch_bounds__(kIncThreads) k_inc_iter(DevGame g) {
         }
         gbar(ctl);
     }
-    const int64_t ne = (int64_t)bcast_ld(&ctl->nE);
-    const bool ovf = bcast_ld(&ctl->inc_overflow) != 0;
+    unsigned long long ev[2];
+    bcast_ld_n<2>({&ctl->nE, &ctl->inc_overflow}, ev);
+    const int64_t ne = (int64_t)ev[0];
+    const bool ovf = ev[1] != 0;
     trace_ts(g, 5);
 
     // ---- 5-7. All_Odd over E: prefix pass, hard pass, apply
@@ -1933,7 +1955,9 @@ __global__ void __launch_bounds__(kIncThreads) k_inc_iter(DevGame g) {
     }
     gbar(ctl);
     trace_ts(g, 6);
-    const int64_t nh = ovf ? 0 : (int64_t)bcast_ld(&ctl->nhard);
+    unsigned long long hv[2];
+    bcast_ld_n<2>({&ctl->nhard, &ctl->nswl}, hv);
+    const int64_t nh = ovf ? 0 : (int64_t)hv[0];
     for (int64_t i = tid; i < nh; i += stride) {
         const int64_t v = __ldcg(g.hard + i);
         int32_t best = -1;
@@ -1944,7 +1968,7 @@ __global__ void __launch_bounds__(kIncThreads) k_inc_iter(DevGame g) {
     if (nh > 0) gbar(ctl);   // (no hard vertex: the switch list is final since the last barrier)
     trace_ts(g, 7);
     // the switch list is final here: its length is this step's switch count (the loop test)
-    const int64_t nsn = (int64_t)bcast_ld(&ctl->nswl);
+    const int64_t nsn = nh > 0 ? (int64_t)bcast_ld(&ctl->nswl) : (int64_t)hv[1];   // (the hard pass appends)
     const int64_t nsl = g.sharded ? 0 : nsn;
     for (int64_t i = tid; i < nsl; i += stride) {   // sharded: applied after the exchange
         const int2 e = __ldcg(g.swl + i);
@@ -2021,7 +2045,9 @@ __global__ void __launch_bounds__(kIncThreads) k_inc_iter(DevGame g) {
         if (rr == 2) g.hard[atomicAdd(&ctl->nhard, 1ull)] = (int32_t)v;
     }
     gbar(ctl);
-    const int64_t nhe = (int64_t)bcast_ld(&ctl->nhard);
+    unsigned long long hev[2];
+    bcast_ld_n<2>({&ctl->nhard, &ctl->nswl}, hev);
+    const int64_t nhe = (int64_t)hev[0];
     for (int64_t i = tid; i < nhe; i += stride) {
         const int64_t v = __ldcg(g.hard + i);
         int32_t best = -1;
@@ -2029,7 +2055,8 @@ __global__ void __launch_bounds__(kIncThreads) k_inc_iter(DevGame g) {
         append_switch(g, rr == 1, v, best);
     }
     if (nhe > 0) gbar(ctl);
-    const int64_t nes = (int64_t)bcast_ld(&ctl->nswl);   // σ := σ[All_Even]; it is S of the next step
+    // σ := σ[All_Even]; it is S of the next step (the hard pass appends to the list)
+    const int64_t nes = nhe > 0 ? (int64_t)bcast_ld(&ctl->nswl) : (int64_t)hev[1];
     for (int64_t i = tid; i < nes; i += stride) {
         const int2 e = __ldcg(g.swl + i);
         g.succ[e.x] = e.y;
