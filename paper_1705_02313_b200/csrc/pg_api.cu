@@ -1175,7 +1175,10 @@ pg_status pg_load(int64_t n, const int64_t *row_ptr, const int32_t *col, const u
     G.inc_blk_frontier = getenv("PGSI_INC_BLK") ? atoi(getenv("PGSI_INC_BLK")) : 256;
     G.inc_closure = getenv("PGSI_INC_CLOSURE") ? atoi(getenv("PGSI_INC_CLOSURE")) : 1;
     G.inc_clo_cap = getenv("PGSI_INC_CLO_CAP") ? std::max(1, atoi(getenv("PGSI_INC_CLO_CAP"))) : 1 << 30;
-    G.inc_split_min = getenv("PGSI_INC_SPLIT") ? atoll(getenv("PGSI_INC_SPLIT")) : 131072;
+    // big steps continued in full-occupancy kernels from this |D| on (0 = never). Measured
+    // (DESIGN.md §V-inc): never at config 3 (n' = 13M), from |D| >= 2^20 on for n' >= 2^25
+    G.inc_split_min = getenv("PGSI_INC_SPLIT") ? atoll(getenv("PGSI_INC_SPLIT"))
+                                               : (G.n_int >= (int64_t(1) << 25) ? (int64_t(1) << 20) : 0);
     G.lvlog = nullptr;
     if (trace_levels) {
         CKL(dalloc(h, &G.lvlog, 8192));

@@ -400,6 +400,8 @@ cudaError_t build_loop_graph(const DevGame &g, const LaunchCfg &lc, const LoopCf
     for (int k = 0; k < 4 && !(omit & 1); k++) {   // incremental launches, one grid class each
         const int64_t nS = (int64_t)cfg.grid_class[k] * kIncThreads / std::max(1, cfg.inc_grid_mul);
         GCK(capture(cs, mb[k], [&] { return launch_inc_iter(g, lc, cs, std::max<int64_t>(1, nS)); }));
+        count += 1;
+        if (g.inc_split_min <= 0) continue;   // big steps stay in k_inc_iter (the default)
         // then IF (ctl->split) { the big-step continuation, launch_inc_split }
         cudaGraphNode_t kn;
         size_t nn = 1;
@@ -411,7 +413,7 @@ cudaError_t build_loop_graph(const DevGame &g, const LaunchCfg &lc, const LoopCf
         std::vector<cudaGraph_t> sb;
         GCK(add_cond(mb[k], &gate, 1, h_split[k], cudaGraphCondTypeIf, 1, &ifn, sb));
         GCK(capture(cs, sb[0], [&] { return launch_inc_split(g, cs); }));
-        count += 2 + 5;
+        count += 1 + 5;
     }
     GCK(capture(cs, mb[LM_FULL], [&] {
         int launches = 0;

@@ -45,7 +45,7 @@ def check(pg, g, ora, **kw):
     {"PGSI_V2_DESIGN": "W"},                       # V2 by Wyllie over full rows (design comparison)
     {"PGSI_INC_SPLIT": "1"},                       # every step continues in launch_inc_split
     {"PGSI_INC_SPLIT": "1", "PGSI_DEVICE_LOOP": "2"},   # ... inside the device graph (IF node)
-    {"PGSI_INC_SPLIT": "0"},                       # never
+    {"PGSI_INC_SPLIT": "131072"},                  # big steps only (the round-2 interim default)
     {"PGSI_INC_EVEN": "0", "PGSI_DEVICE_LOOP": "2"},   # All_Even never inside k_inc_iter
     {"PGSI_INC_STEPS": "3", "PGSI_DEVICE_LOOP": "2"},  # in-kernel All_Even cut short by the step budget
     {"PGSI_INC_CLOSURE": "0"},                     # level-synchronous closure (grid barrier per level)
