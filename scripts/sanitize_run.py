@@ -1,6 +1,7 @@
 """One solve (plus a valuation and a best response) through the C ABI, checked
 against the oracle, for compute-sanitizer runs (scripts/sanitize.sh).
-Usage: python scripts/sanitize_run.py N D [multikernel]"""
+Usage: python scripts/sanitize_run.py N D [multikernel|cluster [devloop]]
+(devloop: the solve runs as the device-resident CUDA graph, PGSI_DEVICE_LOOP=2)"""
 import os
 import sys
 
@@ -13,6 +14,8 @@ if len(sys.argv) > 3 and sys.argv[3] in ("multikernel", "cluster"):
     os.environ["PGSI_SMALL_MAX"] = "0"
     os.environ["PGSI_HOST_LOAD_MAX"] = "0"
     os.environ["PGSI_CLUSTER"] = "0" if sys.argv[3] == "multikernel" else "2"
+if len(sys.argv) > 4 and sys.argv[4] == "devloop":
+    os.environ["PGSI_DEVICE_LOOP"] = "2"
 import pg_inputs as gi  # noqa: E402
 from oracle import Oracle  # noqa: E402
 from paper_1705_02313_b200 import Game  # noqa: E402
