@@ -803,28 +803,38 @@ __global__ void __launch_bounds__(kThreads) k_spl_mark(DevGame g) {
     if (__ldcg(&g.ctl->maxdepth) < (unsigned long long)g.K) return;
     const int64_t N = g.n_int;
     const int lane = threadIdx.x & 31;
-    const int64_t wstride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t base = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll; base < N; base += wstride) {
-        int64_t v = base + lane;
-        bool is = false;
-        if (v < N) {
-            unsigned long long e = __ldcg(g.jl + v);
-            uint32_t depth = (uint32_t)(e >> 32);
-            is = (uint32_t)e == (uint32_t)N && depth >= (uint32_t)g.K && depth % (uint32_t)g.K == 0;
+    const uint32_t K = (uint32_t)g.K;
+    // four consecutive (J, len) words per thread (two 16-byte loads), a warp covers 128
+    const int64_t wstride = (int64_t)gridDim.x * blockDim.x * 4;
+    for (int64_t base = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) & ~31ll) * 4; base < N; base += wstride) {
+        const int64_t v0 = base + 4 * lane;
+        unsigned long long e[4] = {0ull, 0ull, 0ull, 0ull};
+        if (v0 + 3 < N) {
+            const ulonglong2 a = __ldcg(reinterpret_cast<const ulonglong2 *>(g.jl + v0));
+            const ulonglong2 b = __ldcg(reinterpret_cast<const ulonglong2 *>(g.jl + v0) + 1);
+            e[0] = a.x; e[1] = a.y; e[2] = b.x; e[3] = b.y;
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; k++) if (v0 + k < N) e[k] = __ldcg(g.jl + v0 + k);
         }
-        unsigned mask = __ballot_sync(FULL, is);
-        if (!mask) continue;
-        int leader = __ffs(mask) - 1;
-        unsigned long long b0 = 0;
-        if (lane == leader) b0 = atomicAdd(&g.ctl->nspl, (unsigned long long)__popc(mask));
-        b0 = __shfl_sync(FULL, b0, leader);
-        if (is) {
-            unsigned long long idx = b0 + __popc(mask & ((1u << lane) - 1));
-            if (idx < (unsigned long long)g.spl_cap) {
-                g.sidx[v] = (int32_t)idx;
-                g.spl[idx] = (int32_t)v;
-            } else {
-                g.ctl->spl_overflow = 1;
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const uint32_t depth = (uint32_t)(e[k] >> 32);
+            const bool is = v0 + k < N && (uint32_t)e[k] == (uint32_t)N && depth >= K && depth % K == 0;
+            const unsigned mask = __ballot_sync(FULL, is);
+            if (!mask) continue;
+            const int leader = __ffs(mask) - 1;
+            unsigned long long b0 = 0;
+            if (lane == leader) b0 = atomicAdd(&g.ctl->nspl, (unsigned long long)__popc(mask));
+            b0 = __shfl_sync(FULL, b0, leader);
+            if (is) {
+                const unsigned long long idx = b0 + __popc(mask & ((1u << lane) - 1));
+                if (idx < (unsigned long long)g.spl_cap) {
+                    g.sidx[v0 + k] = (int32_t)idx;
+                    g.spl[idx] = (int32_t)(v0 + k);
+                } else {
+                    g.ctl->spl_overflow = 1;
+                }
             }
         }
     }
