@@ -2519,6 +2519,13 @@ cudaError_t launch_cycle_dom(const DevGame &g, const LaunchCfg &lc, cudaStream_t
     return coop((const void *)k_cycle_dom, lc.coop_cyc, args, s);
 }
 
+// The hard pass handles the few vertices whose prefix compares were undecided (0-2 per
+// step at config 3): a small grid keeps the mostly empty launch cheap.
+#ifndef PGSI_HARD_GRID_DIV
+#define PGSI_HARD_GRID_DIV 4
+#endif
+static int hard_grid() { return std::max(1, g_lc.sms / PGSI_HARD_GRID_DIV); }
+
 cudaError_t launch_switch(const DevGame &g, bool odd, cudaStream_t s) {
     const int64_t nv = odd ? g.n_int - g.n_even : g.n_even;
     if (nv <= 0) return cudaSuccess;
@@ -2529,7 +2536,7 @@ cudaError_t launch_switch(const DevGame &g, bool odd, cudaStream_t s) {
     else k_switch<false, false><<<grid, kThreads, 0, s>>>(g, nullptr);
     e = cudaGetLastError();
     if (e) return e;
-    const int hgrid = std::max(1, g_lc.sms * 2);
+    const int hgrid = hard_grid();
     if (odd) k_switch<true, true><<<hgrid, kThreads, 0, s>>>(g, nullptr);
     else k_switch<false, true><<<hgrid, kThreads, 0, s>>>(g, nullptr);
     e = cudaGetLastError();
@@ -2565,7 +2572,7 @@ cudaError_t launch_apply_all(const DevGame &g, cudaStream_t s) {
 cudaError_t launch_inc_split(const DevGame &g, cudaStream_t s) {
     k_inc_v2_split<<<grid_for(g.n_int / 8 + 1, kThreads, 16), kThreads, 0, s>>>(g);
     k_switch<true, false><<<std::max(1, g_lc.sms * 4), kThreads, 0, s>>>(g, g.El);
-    k_switch<true, true><<<std::max(1, g_lc.sms * 2), kThreads, 0, s>>>(g, nullptr);
+    k_switch<true, true><<<hard_grid(), kThreads, 0, s>>>(g, nullptr);
     k_apply_switches<<<std::max(1, g_lc.sms * 4), kThreads, 0, s>>>(g, 0);
     k_inc_split_fin<<<1, 1, 0, s>>>(g.ctl);
     return cudaGetLastError();
@@ -2579,7 +2586,7 @@ cudaError_t launch_even_inc(const DevGame &g, cudaStream_t s) {
     const int grid = std::max(1, g_lc.sms * 4);
     k_ebuild_even<<<grid, kThreads, 0, s>>>(g);
     k_switch<false, false><<<grid, kThreads, 0, s>>>(g, g.El);
-    k_switch<false, true><<<std::max(1, g_lc.sms * 2), kThreads, 0, s>>>(g, nullptr);
+    k_switch<false, true><<<hard_grid(), kThreads, 0, s>>>(g, nullptr);
     k_apply_switches<<<grid, kThreads, 0, s>>>(g, 0);
     return cudaGetLastError();
 }
