@@ -211,13 +211,23 @@ __global__ void kl_fill(int64_t n, int64_t n_int, const int32_t *iperm, const in
     }
 }
 
-__global__ void kl_indeg(int64_t m, const int32_t *col, uint32_t *indeg) {
-    GS_LOOP(e, m) atomicAdd(indeg + col[e], 1u);
+// Reverse CSR by a stable radix sort of the (target, source) edge pairs: src[e] = the
+// source of edge e (nondecreasing in e), then rcol = the sources sorted by target, so each
+// reverse row lists its predecessors in ascending order, as the host transform does. (An
+// atomic-cursor fill measured 1.6 ms at config 3: scattered 4-byte writes cost a DRAM
+// read-modify-write each.)
+__global__ void kl_edge_src(int64_t n_int, const uint32_t *rp, int32_t *src) {
+    GS_LOOP(u, n_int) {
+        for (uint32_t e = rp[u]; e < rp[u + 1]; e++) src[e] = (int32_t)u;
+    }
 }
 
-__global__ void kl_rev_fill(int64_t n_int, const uint32_t *rp, const int32_t *col, uint32_t *cursor, int32_t *rcol) {
-    GS_LOOP(u, n_int) {
-        for (uint32_t e = rp[u]; e < rp[u + 1]; e++) rcol[atomicAdd(cursor + col[e], 1u)] = (int32_t)u;
+// rrp[v] = first position of target v in the sorted targets (= m for targets past the last)
+__global__ void kl_rrp_from_keys(int64_t n_int, int64_t m, const int32_t *keys, uint32_t *rrp) {
+    GS_LOOP(e, m + 1) {
+        const int64_t lo = e == 0 ? -1 : (int64_t)keys[e - 1];
+        const int64_t hi = e == m ? n_int : (int64_t)keys[e];
+        for (int64_t v = lo + 1; v <= hi; v++) rrp[v] = (uint32_t)e;
     }
 }
 
@@ -447,14 +457,23 @@ pg_status build_device_game(int64_t n, const int64_t *row_ptr, const int32_t *co
     uint32_t *rrp = (uint32_t *)persist(4 * N1);
     int32_t *rcol = (int32_t *)persist(4 * std::max<uint32_t>(m_int, 1));
     if (!rrp || !rcol) { err = "device allocation failed"; return PG_ENOMEM; }
-    uint32_t *d_indeg, *d_cur2;
-    CKD(sc.get(&d_indeg, N1));
-    CKD(sc.get(&d_cur2, N1));
-    CKD(cudaMemsetAsync(d_indeg, 0, 4 * N1, s));
-    if (m_int) kl_indeg<<<grid1(m_int), T, 0, s>>>(m_int, dcol, d_indeg);
-    CKD(exscan(d_indeg, rrp, N1, s));
-    CKD(cudaMemcpyAsync(d_cur2, rrp, 4 * N1, cudaMemcpyDeviceToDevice, s));
-    if (n_int) kl_rev_fill<<<grid1(n_int), T, 0, s>>>(n_int, rp, dcol, d_cur2, rcol);
+    {
+        int32_t *d_src, *d_keys;
+        CKD(sc.get(&d_src, std::max<int64_t>(m_int, 1)));
+        CKD(sc.get(&d_keys, std::max<int64_t>(m_int, 1)));
+        if (n_int) kl_edge_src<<<grid1(n_int), T, 0, s>>>(n_int, rp, d_src);
+        int end_bit = 1;
+        while (end_bit < 32 && (int64_t(1) << end_bit) < n_int) end_bit++;
+        size_t bytes = 0;
+        CKD(cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const int32_t *)dcol, d_keys, (const int32_t *)d_src, rcol,
+                                            (int64_t)m_int, 0, end_bit, s));
+        void *tmp = nullptr;
+        CKD(sc.get((char **)&tmp, std::max<size_t>(bytes, 16)));
+        if (m_int)
+            CKD(cub::DeviceRadixSort::SortPairs(tmp, bytes, (const int32_t *)dcol, d_keys, (const int32_t *)d_src, rcol,
+                                                (int64_t)m_int, 0, end_bit, s));
+        kl_rrp_from_keys<<<grid1(m_int + 1), T, 0, s>>>(n_int, (int64_t)m_int, d_keys, rrp);
+    }
     CKD(cudaGetLastError());
     CKD(cudaStreamSynchronize(s));
     out.n_int = n_int;
