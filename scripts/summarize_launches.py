@@ -32,11 +32,15 @@ for i, m in launch.items():
     a[1] += m.get("gpu__time_duration.sum", 0) * 1e-6   # ns -> ms
     a[2] += m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)
     a[3] += m.get("lts__t_sector_hit_rate.pct", 0)
-tot = sum(a[1] for k, a in agg.items() if not k.startswith("kl_"))
+def is_load(k):   # the load transform: its own kernels and the CUB sorts / scans / partitions it calls
+    return k.startswith("kl_") or "cub::" in k
+
+
+tot = sum(a[1] for k, a in agg.items() if not is_load(k))
 print(f"{'kernel':42s} {'n':>5s} {'ms':>8s} {'share':>6s} {'avg_us':>8s} {'MB/launch':>10s} {'GB/s':>7s} {'L2hit%':>6s}")
 for k, a in sorted(agg.items(), key=lambda x: -x[1][1]):
     n, ms, b, l2 = a
-    share = "" if k.startswith("kl_") else f"{100 * ms / tot:5.1f}%"
+    share = "" if is_load(k) else f"{100 * ms / tot:5.1f}%"
     print(f"{k[:42]:42s} {n:5d} {ms:8.3f} {share:>6s} {1e3 * ms / n:8.1f} {b / n / 1e6:10.1f} "
           f"{b / (ms * 1e-3) / 1e9 if ms else 0:7.0f} {l2 / n:6.1f}")
-print(f"solve kernels total (excl. kl_* load transform): {tot:.3f} ms")
+print(f"solve kernels total (excl. the load transform: kl_* and CUB): {tot:.3f} ms")
