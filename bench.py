@@ -429,6 +429,12 @@ def main():
                 "bytes_per_launch": dbytes / max(dn, 1), "ms_per_launch": dms / max(dn, 1),
                 "share_of_step": dms / total_phase_ms if total_phase_ms else None,
                 "peak_source": peak_src,
+                # context: the kernel's actual DRAM rate against the measured ceiling of random
+                # 8-byte gathers from a DRAM-resident table (each fills a 128-byte line)
+                "dram_actual_GBps": (traffic / (dms / max(dn, 1) / 1000.0) / 1e9) if (traffic and dms) else None,
+                "random_gather_ceiling_GBps": 5006.0,
+                "random_gather_ceiling_source": "scripts/micro/gather_bw.cu, profiles/r2/micro/gather_bw_ncu.txt "
+                                                "(7.88 GB of DRAM reads in 1.573 ms for 64 Mi random 8-byte gathers)",
                 "timing": "CUDA events around each phase on the library's stream, over the same number "
                           "of solves of this game with PG_PHASE_TIMING (host-driven loop) right after "
                           f"the timed region ({host_loop_ms:.2f} ms per solve that way)",
