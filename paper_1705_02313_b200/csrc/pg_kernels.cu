@@ -276,13 +276,23 @@ __device__ __forceinline__ void hist_add(uint32_t (&h)[NW], uint32_t p) {
     for (int q = 0; q < NW; q++) h[q] += (w == (uint32_t)q) ? inc : 0u;
 }
 
-// Walk `steps` successors from x, counting priorities in [lo, lo + 4*NW).
+// Walk `steps` successors from x, counting priorities in [lo, lo + 4*NW). Two steps per
+// dependent load through V1's s2p words (callers run in the valuation whose V1 wrote them,
+// and never walk past the sink: steps <= depth).
 template <int NW>
 __device__ __forceinline__ int32_t walk(const DevGame &g, int32_t x, uint32_t steps, uint32_t lo,
                                         uint32_t (&h)[NW]) {
-    for (uint32_t s = 0; s < steps; s++) {
-        uint32_t p = (uint32_t)__ldg(g.pidx + x) - lo;
-        int32_t nx = __ldg(g.succ + x);
+    uint32_t s = 0;
+    for (; s + 2 <= steps; s += 2) {
+        const unsigned long long w = __ldg(g.s2p + x);
+        const uint32_t p1 = ((uint32_t)(w >> 32) & 0xffu) - lo, p2 = ((uint32_t)(w >> 40) & 0xffu) - lo;
+        if (p1 < 4u * NW) hist_add<NW>(h, p1);
+        if (p2 < 4u * NW) hist_add<NW>(h, p2);
+        x = (int32_t)(uint32_t)w;
+    }
+    if (s < steps) {
+        const uint32_t p = (uint32_t)__ldg(g.pidx + x) - lo;
+        const int32_t nx = __ldg(g.succ + x);
         if (p < 4u * NW) hist_add<NW>(h, p);
         x = nx;
     }
