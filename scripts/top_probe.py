@@ -13,7 +13,6 @@ g = gi.random_game(*a)
 G = Game.from_game(g, trace=True)
 r = G.solve()
 t = G.get_trace()
-n = G.info()["n_internal"] if hasattr(G, "info") else None
 for row in t:
     print(int(row[0]), int(row[3]), int(row[4]))
 print({k: r.stats[k] for k in ("inner_iters", "outer_passes", "top_vertices") if k in r.stats})
